@@ -1,0 +1,1829 @@
+// Host side of the B200 transport sweep: problem ingestion, mesh face pairing,
+// exact face geometry, per-element operator tensors, per-ordinate couplings,
+// dependency graphs, cut sets, orderings, levels and worklists, and the C ABI
+// declared in include/hosweep_b200.h.
+//
+// Reference mapping (paths under /root/reference/proj/include/hosweep/):
+//   quadrature.hpp:23-104  -> gauss_legendre / gauss_lobatto / tensor rule
+//   basis.hpp:15-133       -> Lagrange1D / TensorBasis
+//   mesh.hpp:121-365       -> Mesh::build_faces / jacobian / face_geometry / checks
+//   assembly.hpp:58-163    -> element_tensors (M, G_k = -(d_k u)^T W u; the per-ordinate
+//                             stream block is sum_k Omega_k G_k, assembled on the GPU)
+//   assembly.hpp:185-268   -> face_couplings (Gauss face rule, shared sampling,
+//                             edge threshold 1e-12*length) — bit-exact with the reference
+//                             element-wise arithmetic so the graph is bit-exact
+//   sweepgraph.hpp:54-396  -> build_graph / tarjan_scc / min_fas_* / sweep_ordering
+//   solver.hpp:52-168      -> hsw_create (ctor), hsw_sweep, hsw_source_iteration
+//   solver.hpp:220-245     -> hsw_balance
+// Compiled with -ffp-contract=off: every quantity that feeds an integer
+// decision is evaluated with the reference's operation order.
+#include "hosweep_b200.h"
+#include "hsw_internal.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <queue>
+#include <thread>
+#include <vector>
+
+namespace hsw {
+
+// ------------------------------------------------------------------ threads
+static int host_workers() {
+    if (const char* env = std::getenv("HOSWEEP_THREADS")) {  // parallel.hpp:16-23
+        const int n = std::atoi(env);
+        if (n >= 1) return n;
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw == 0 ? 1 : (int)hw;
+}
+
+template <typename Fn>
+static void parallel_for(int64_t n, Fn&& fn) {
+    const int workers = (int)std::min<int64_t>(n, host_workers());
+    if (workers <= 1) {
+        for (int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::exception_ptr error;
+    std::mutex mu;
+    std::atomic<int64_t> next{0};
+    for (int w = 0; w < workers; ++w)
+        pool.emplace_back([&] {
+            for (;;) {
+                const int64_t i = next.fetch_add(1);
+                if (i >= n) return;
+                try {
+                    fn(i);
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (!error) error = std::current_exception();
+                    return;
+                }
+            }
+        });
+    for (auto& t : pool) t.join();
+    if (error) std::rethrow_exception(error);
+}
+
+// ----------------------------------------------------------------- numerics
+static void legendre(int n, double x, double& p, double& dp) {  // quadrature.hpp:23-34
+    double p0 = 1.0, p1 = x;
+    if (n == 0) { p = p0; dp = 0.0; return; }
+    for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+    }
+    p = p1;
+    dp = n * (x * p1 - p0) / (x * x - 1.0);
+}
+
+struct Rule { std::vector<double> x, w; };
+
+static Rule gauss_legendre(int n) {  // quadrature.hpp:38-59
+    if (n < 1) throw Error(HSW_ERR_INVALID, "gauss_legendre: need n >= 1");
+    Rule r;
+    r.x.resize(n);
+    r.w.resize(n);
+    for (int i = 0; i < n; ++i) {
+        double x = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+        double p = 0.0, dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            legendre(n, x, p, dp);
+            const double dx = p / dp;
+            x -= dx;
+            if (std::abs(dx) < 1e-15) break;
+        }
+        legendre(n, x, p, dp);
+        r.x[n - 1 - i] = 0.5 * (x + 1.0);
+        r.w[n - 1 - i] = 1.0 / ((1.0 - x * x) * dp * dp);
+    }
+    return r;
+}
+
+static std::vector<double> gauss_lobatto(int n) {  // quadrature.hpp:62-82
+    std::vector<double> pts(n);
+    pts.front() = 0.0;
+    pts.back() = 1.0;
+    const int m = n - 1;
+    for (int i = 1; i < m; ++i) {
+        double x = std::cos(M_PI * i / m);
+        for (int it = 0; it < 100; ++it) {
+            double p, dp;
+            legendre(m, x, p, dp);
+            const double ddp = (2.0 * x * dp - m * (m + 1) * p) / (1.0 - x * x);
+            const double dx = dp / ddp;
+            x -= dx;
+            if (std::abs(dx) < 1e-15) break;
+        }
+        pts[m - i] = 0.5 * (x + 1.0);
+    }
+    return pts;
+}
+
+// Lagrange1D product form (basis.hpp:15-60) and the tensor basis
+// (basis.hpp:62-133, 3D: m = (iz*n1 + iy)*n1 + ix, value (vx*vy)*vz).
+struct TensorBasis {
+    int dim = 2, order = 1, n1 = 2, nb = 4;
+    std::vector<double> nodes;
+    TensorBasis() = default;
+    TensorBasis(int d, int p) : dim(d), order(p), n1(p + 1) {
+        nodes = gauss_lobatto(p + 1);
+        nb = d == 2 ? n1 * n1 : n1 * n1 * n1;
+    }
+    double value(int j, double x) const {
+        double v = 1.0;
+        for (int k = 0; k < n1; ++k) {
+            if (k == j) continue;
+            v *= (x - nodes[k]) / (nodes[j] - nodes[k]);
+        }
+        return v;
+    }
+    double derivative(int j, double x) const {
+        double d = 0.0;
+        for (int i = 0; i < n1; ++i) {
+            if (i == j) continue;
+            double term = 1.0 / (nodes[j] - nodes[i]);
+            for (int k = 0; k < n1; ++k) {
+                if (k == j || k == i) continue;
+                term *= (x - nodes[k]) / (nodes[j] - nodes[k]);
+            }
+            d += term;
+        }
+        return d;
+    }
+    void values(const double* xi, double* out) const {
+        double vx[32], vy[32], vz[32];
+        for (int j = 0; j < n1; ++j) { vx[j] = value(j, xi[0]); vy[j] = value(j, xi[1]); }
+        if (dim == 2) {
+            for (int iy = 0; iy < n1; ++iy)
+                for (int ix = 0; ix < n1; ++ix) out[iy * n1 + ix] = vx[ix] * vy[iy];
+            return;
+        }
+        for (int j = 0; j < n1; ++j) vz[j] = value(j, xi[2]);
+        for (int iz = 0; iz < n1; ++iz)
+            for (int iy = 0; iy < n1; ++iy)
+                for (int ix = 0; ix < n1; ++ix) out[(iz * n1 + iy) * n1 + ix] = vx[ix] * vy[iy] * vz[iz];
+    }
+    void gradients(const double* xi, double* out) const {  // out[m*dim + k]
+        double vx[32], vy[32], vz[32], dx[32], dy[32], dz[32];
+        for (int j = 0; j < n1; ++j) {
+            vx[j] = value(j, xi[0]); vy[j] = value(j, xi[1]);
+            dx[j] = derivative(j, xi[0]); dy[j] = derivative(j, xi[1]);
+        }
+        if (dim == 2) {
+            for (int iy = 0; iy < n1; ++iy)
+                for (int ix = 0; ix < n1; ++ix) {
+                    const int m = iy * n1 + ix;
+                    out[2 * m] = dx[ix] * vy[iy];
+                    out[2 * m + 1] = vx[ix] * dy[iy];
+                }
+            return;
+        }
+        for (int j = 0; j < n1; ++j) { vz[j] = value(j, xi[2]); dz[j] = derivative(j, xi[2]); }
+        for (int iz = 0; iz < n1; ++iz)
+            for (int iy = 0; iy < n1; ++iy)
+                for (int ix = 0; ix < n1; ++ix) {
+                    const int m = (iz * n1 + iy) * n1 + ix;
+                    out[3 * m] = dx[ix] * vy[iy] * vz[iz];
+                    out[3 * m + 1] = vx[ix] * dy[iy] * vz[iz];
+                    out[3 * m + 2] = vx[ix] * vy[iy] * dz[iz];
+                }
+    }
+};
+
+// --------------------------------------------------------- reference faces
+// 2D: mesh.hpp:64-109.  3D: 0 z=0 (s,t,0); 1 y=0 (s,0,t); 2 x=1 (1,s,t);
+// 3 y=1 (s,1,t); 4 x=0 (0,s,t); 5 z=1 (s,t,1).  DESIGN.md §3.
+static int nfaces_of(int dim) { return dim == 2 ? 4 : 6; }
+
+static void param_point(int dim, int f, double s, double t, double* xi) {
+    xi[2] = 0.0;
+    if (dim == 2) {
+        static const double fix[4][2] = {{-1, 0}, {1, -1}, {-1, 1}, {0, -1}};
+        (void)fix;
+        switch (f) {
+            case 0: xi[0] = s; xi[1] = 0.0; return;
+            case 1: xi[0] = 1.0; xi[1] = s; return;
+            case 2: xi[0] = s; xi[1] = 1.0; return;
+            default: xi[0] = 0.0; xi[1] = s; return;
+        }
+    }
+    switch (f) {
+        case 0: xi[0] = s; xi[1] = t; xi[2] = 0.0; return;
+        case 1: xi[0] = s; xi[1] = 0.0; xi[2] = t; return;
+        case 2: xi[0] = 1.0; xi[1] = s; xi[2] = t; return;
+        case 3: xi[0] = s; xi[1] = 1.0; xi[2] = t; return;
+        case 4: xi[0] = 0.0; xi[1] = s; xi[2] = t; return;
+        default: xi[0] = s; xi[1] = t; xi[2] = 1.0; return;
+    }
+}
+static void face_axes(int dim, int f, int& a0, int& a1) {
+    if (dim == 2) { a0 = (f == 0 || f == 2) ? 0 : 1; a1 = -1; return; }
+    if (f == 0 || f == 5) { a0 = 0; a1 = 1; }
+    else if (f == 1 || f == 3) { a0 = 0; a1 = 2; }
+    else { a0 = 1; a1 = 2; }
+}
+static void ref_normal(int dim, int f, double* n) {
+    n[0] = n[1] = n[2] = 0.0;
+    if (dim == 2) {
+        static const double t[4][2] = {{0, -1}, {1, 0}, {0, 1}, {-1, 0}};
+        n[0] = t[f][0]; n[1] = t[f][1];
+        return;
+    }
+    static const double t[6][3] = {{0, 0, -1}, {0, -1, 0}, {1, 0, 0}, {0, 1, 0}, {-1, 0, 0}, {0, 0, 1}};
+    n[0] = t[f][0]; n[1] = t[f][1]; n[2] = t[f][2];
+}
+static std::vector<int> face_nodes(int dim, int f, int order) {
+    const int n1 = order + 1;
+    std::vector<int> idx;
+    if (dim == 2) {
+        for (int k = 0; k < n1; ++k) {
+            switch (f) {
+                case 0: idx.push_back(k); break;
+                case 1: idx.push_back(order + k * n1); break;
+                case 2: idx.push_back(order * n1 + k); break;
+                default: idx.push_back(k * n1); break;
+            }
+        }
+        return idx;
+    }
+    for (int b = 0; b < n1; ++b)
+        for (int a = 0; a < n1; ++a) {
+            int ix, iy, iz;
+            switch (f) {
+                case 0: ix = a; iy = b; iz = 0; break;
+                case 1: ix = a; iy = 0; iz = b; break;
+                case 2: ix = order; iy = a; iz = b; break;
+                case 3: ix = a; iy = order; iz = b; break;
+                case 4: ix = 0; iy = a; iz = b; break;
+                default: ix = a; iy = b; iz = order; break;
+            }
+            idx.push_back((iz * n1 + iy) * n1 + ix);
+        }
+    return idx;
+}
+static void orient_param(int dim, int code, double s, double t, double& so, double& to) {
+    if (dim == 2) { so = code ? 1.0 - s : s; to = 0.0; return; }
+    double u = s, v = t;
+    if (code & 4) { u = t; v = s; }
+    if (code & 2) u = 1.0 - u;
+    if (code & 1) v = 1.0 - v;
+    so = u; to = v;
+}
+static void orient_index(int dim, int code, int r, int a, int b, int& ao, int& bo) {
+    if (dim == 2) { ao = code ? r - a : a; bo = 0; return; }
+    int u = a, v = b;
+    if (code & 4) { u = b; v = a; }
+    if (code & 2) u = r - u;
+    if (code & 1) v = r - v;
+    ao = u; bo = v;
+}
+static int orient_inverse(int dim, int code) {
+    if (dim == 2) return code;
+    for (int c = 0; c < 8; ++c) {
+        bool ok = true;
+        for (int a = 0; a < 3 && ok; ++a)
+            for (int b = 0; b < 3 && ok; ++b) {
+                int a1, b1, a2, b2;
+                orient_index(3, code, 2, a, b, a1, b1);
+                orient_index(3, c, 2, a1, b1, a2, b2);
+                if (a2 != a || b2 != b) ok = false;
+            }
+        if (ok) return c;
+    }
+    return code;
+}
+
+// --------------------------------------------------------------------- mesh
+struct IFace { int el, er, fl, fr, orient; };
+struct BFace { int elem, face, attr; };
+
+struct Mesh {
+    int dim = 2, order = 1, npe = 4;
+    TensorBasis geom;
+    std::vector<double> pts;  // P * dim
+    std::vector<int> enodes;  // E * npe
+    std::vector<int> region;
+    std::vector<BFace> bfaces;
+    std::vector<IFace> ifaces;
+    int nel = 0;
+
+    const double* X(int e, int m) const { return &pts[(size_t)enodes[(size_t)e * npe + m] * dim]; }
+
+    // mesh.hpp:157-170 with a precomputed gradient table g (npe*dim) at xi
+    double jacobian_tab(int e, const double* g, double* J) const {
+        for (int i = 0; i < 9; ++i) J[i] = 0.0;
+        for (int m = 0; m < npe; ++m) {
+            const double* x = X(e, m);
+            for (int a = 0; a < dim; ++a)
+                for (int b = 0; b < dim; ++b) J[a * 3 + b] += x[a] * g[m * dim + b];
+        }
+        return det(J);
+    }
+    double det(const double* J) const {
+        if (dim == 2) return J[0] * J[4] - J[3] * J[1];
+        const double c0 = J[4] * J[8] - J[5] * J[7];
+        const double c1 = J[5] * J[6] - J[3] * J[8];
+        const double c2 = J[3] * J[7] - J[4] * J[6];
+        return J[0] * c0 + J[1] * c1 + J[2] * c2;
+    }
+    void inverse(const double* J, double* K) const {
+        if (dim == 2) {
+            const double invdet = 1.0 / (J[0] * J[4] - J[3] * J[1]);
+            K[0] = J[4] * invdet;
+            K[3] = -J[3] * invdet;
+            K[1] = -J[1] * invdet;
+            K[4] = J[0] * invdet;
+            return;
+        }
+        const double c00 = J[4] * J[8] - J[5] * J[7];
+        const double c01 = J[5] * J[6] - J[3] * J[8];
+        const double c02 = J[3] * J[7] - J[4] * J[6];
+        const double invdet = 1.0 / (J[0] * c00 + J[1] * c01 + J[2] * c02);
+        K[0] = c00 * invdet;
+        K[1] = (J[2] * J[7] - J[1] * J[8]) * invdet;
+        K[2] = (J[1] * J[5] - J[2] * J[4]) * invdet;
+        K[3] = c01 * invdet;
+        K[4] = (J[0] * J[8] - J[2] * J[6]) * invdet;
+        K[5] = (J[2] * J[3] - J[0] * J[5]) * invdet;
+        K[6] = c02 * invdet;
+        K[7] = (J[1] * J[6] - J[0] * J[7]) * invdet;
+        K[8] = (J[0] * J[4] - J[1] * J[3]) * invdet;
+    }
+    void map_tab(int e, const double* v, double* x) const {  // mesh.hpp:147-154
+        x[0] = x[1] = x[2] = 0.0;
+        for (int m = 0; m < npe; ++m) {
+            const double* p = X(e, m);
+            for (int a = 0; a < dim; ++a) x[a] += v[m] * p[a];
+        }
+    }
+    double diameter(int e) const {  // mesh.hpp:204-217
+        const int r = order, n1 = r + 1;
+        std::vector<int> c;
+        if (dim == 2) c = {0, r, r * n1, r * n1 + r};
+        else
+            for (int cz : {0, r})
+                for (int cy : {0, r})
+                    for (int cx : {0, r}) c.push_back((cz * n1 + cy) * n1 + cx);
+        double d = 0.0;
+        for (size_t i = 0; i < c.size(); ++i)
+            for (size_t j = i + 1; j < c.size(); ++j) {
+                double s = 0.0;
+                for (int a = 0; a < dim; ++a) {
+                    const double df = X(e, c[i])[a] - X(e, c[j])[a];
+                    s += df * df;
+                }
+                d = std::max(d, std::sqrt(s));
+            }
+        return d;
+    }
+    // mesh.hpp:180-200 given the geometry gradient table at the face point
+    void face_geometry_tab(int e, int f, const double* g, double* normal, double& sj) const {
+        double J[9];
+        jacobian_tab(e, g, J);
+        int a0, a1;
+        face_axes(dim, f, a0, a1);
+        if (dim == 2) {
+            const double t0 = J[a0], t1 = J[3 + a0];
+            sj = std::sqrt(t0 * t0 + t1 * t1);
+        } else {
+            const double u0 = J[a0], u1 = J[3 + a0], u2 = J[6 + a0];
+            const double v0 = J[a1], v1 = J[3 + a1], v2 = J[6 + a1];
+            const double c0 = u1 * v2 - u2 * v1;
+            const double c1 = u2 * v0 - u0 * v2;
+            const double c2 = u0 * v1 - u1 * v0;
+            sj = std::sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+        }
+        if (sj < 1e-14 * diameter(e))
+            throw Error(HSW_ERR_GEOMETRY, "face_geometry: degenerate tangent on element " +
+                                              std::to_string(e) + " face " + std::to_string(f));
+        double K[9], nref[3];
+        inverse(J, K);
+        ref_normal(dim, f, nref);
+        double z = 0.0;
+        for (int i = 0; i < dim; ++i) {
+            double v = 0.0;
+            for (int j = 0; j < dim; ++j) v += K[j * 3 + i] * nref[j];
+            normal[i] = v;
+        }
+        for (int i = 0; i < dim; ++i) z += normal[i] * normal[i];
+        if (z > 0.0) {
+            const double rt = std::sqrt(z);
+            for (int i = 0; i < dim; ++i) normal[i] /= rt;
+        }
+        if (dim == 2) normal[2] = 0.0;
+    }
+    std::vector<int> face_global(int e, int f) const {
+        std::vector<int> out;
+        for (int m : face_nodes(dim, f, order)) out.push_back(enodes[(size_t)e * npe + m]);
+        return out;
+    }
+    // mesh.hpp:242-262
+    void check_connectivity(int num_points) const {
+        for (int e = 0; e < nel; ++e)
+            for (int m = 0; m < npe; ++m) {
+                const int idx = enodes[(size_t)e * npe + m];
+                if (idx < 0 || idx >= num_points)
+                    throw Error(HSW_ERR_MESH, "mesh: element " + std::to_string(e) +
+                                                  " references control point " + std::to_string(idx) +
+                                                  " out of range");
+            }
+        for (const auto& b : bfaces)
+            if (b.elem < 0 || b.elem >= nel || b.face < 0 || b.face >= nfaces_of(dim))
+                throw Error(HSW_ERR_MESH, "mesh: boundary face record (elem " + std::to_string(b.elem) +
+                                              ", face " + std::to_string(b.face) + ") out of range");
+    }
+    // mesh.hpp:275-339; interior-face ids follow the sorted corner keys (std::map order)
+    void build_faces() {
+        const int nf = nfaces_of(dim), r = order, n1 = r + 1;
+        struct Side { std::array<int, 4> key; int e, f; };
+        std::vector<Side> sides;
+        sides.reserve((size_t)nel * nf);
+        for (int e = 0; e < nel; ++e)
+            for (int f = 0; f < nf; ++f) {
+                const auto g = face_global(e, f);
+                std::array<int, 4> key{};
+                if (dim == 2) {
+                    key = {g.front(), g.back(), -1, -1};
+                    if (key[0] > key[1]) std::swap(key[0], key[1]);
+                } else {
+                    key = {g[0], g[r], g[r * n1], g[r * n1 + r]};
+                    std::sort(key.begin(), key.end());
+                }
+                sides.push_back({key, e, f});
+            }
+        std::stable_sort(sides.begin(), sides.end(), [](const Side& a, const Side& b) { return a.key < b.key; });
+        std::vector<char> paired((size_t)nel * nf, 0);
+        ifaces.clear();
+        for (size_t i = 0; i < sides.size();) {
+            size_t j = i;
+            while (j < sides.size() && sides[j].key == sides[i].key) ++j;
+            const size_t cnt = j - i;
+            if (cnt > 2)
+                throw Error(HSW_ERR_MESH, "mesh: face shared by " + std::to_string(cnt) + " elements");
+            if (cnt == 2) {
+                const int e0 = sides[i].e, f0 = sides[i].f, e1 = sides[i + 1].e, f1 = sides[i + 1].f;
+                const auto g0 = face_global(e0, f0), g1 = face_global(e1, f1);
+                int orient = -1;
+                const int ncodes = dim == 2 ? 2 : 8;
+                for (int code = 0; code < ncodes && orient < 0; ++code) {
+                    bool ok = true;
+                    for (int b = 0; b < (dim == 2 ? 1 : n1) && ok; ++b)
+                        for (int a = 0; a < n1 && ok; ++a) {
+                            int ao, bo;
+                            orient_index(dim, code, r, a, b, ao, bo);
+                            if (g1[bo * n1 + ao] != g0[b * n1 + a]) ok = false;
+                        }
+                    if (ok) orient = code;
+                }
+                if (orient < 0)
+                    throw Error(HSW_ERR_MESH, "mesh: elements " + std::to_string(e0) + " and " +
+                                                  std::to_string(e1) +
+                                                  " share face corners but edge nodes do not match");
+                ifaces.push_back({e0, e1, f0, f1, orient});
+                paired[(size_t)e0 * nf + f0] = paired[(size_t)e1 * nf + f1] = 1;
+            }
+            i = j;
+        }
+        std::vector<char> declared((size_t)nel * nf, 0);
+        for (const auto& b : bfaces) {
+            if (paired[(size_t)b.elem * nf + b.face])
+                throw Error(HSW_ERR_MESH, "mesh: boundary record for interior face (elem " +
+                                              std::to_string(b.elem) + ", face " + std::to_string(b.face) + ")");
+            if (declared[(size_t)b.elem * nf + b.face])
+                throw Error(HSW_ERR_MESH, "mesh: duplicate boundary record (elem " + std::to_string(b.elem) +
+                                              ", face " + std::to_string(b.face) + ")");
+            declared[(size_t)b.elem * nf + b.face] = 1;
+        }
+        for (int e = 0; e < nel; ++e)
+            for (int f = 0; f < nf; ++f)
+                if (!paired[(size_t)e * nf + f] && !declared[(size_t)e * nf + f])
+                    throw Error(HSW_ERR_MESH, "mesh: face (elem " + std::to_string(e) + ", face " +
+                                                  std::to_string(f) + ") is neither interior nor declared boundary");
+    }
+};
+
+// ------------------------------------------------------------ sweep graph
+struct Edge { int from, to; double weight; };
+
+// sweepgraph.hpp:82-136
+static std::vector<std::vector<int>> tarjan_scc(int n, const std::vector<Edge>& edges) {
+    std::vector<std::vector<int>> adj(n);
+    for (size_t i = 0; i < edges.size(); ++i) adj[edges[i].from].push_back((int)i);
+    std::vector<int> index(n, -1), low(n, 0), stack;
+    std::vector<char> on(n, 0);
+    std::vector<std::vector<int>> sccs;
+    int next = 0;
+    struct Frame { int v; size_t child; };
+    std::vector<Frame> call;
+    for (int root = 0; root < n; ++root) {
+        if (index[root] != -1) continue;
+        call.push_back({root, 0});
+        index[root] = low[root] = next++;
+        stack.push_back(root);
+        on[root] = 1;
+        while (!call.empty()) {
+            Frame& fr = call.back();
+            if (fr.child < adj[fr.v].size()) {
+                const int w = edges[adj[fr.v][fr.child++]].to;
+                if (index[w] == -1) {
+                    index[w] = low[w] = next++;
+                    stack.push_back(w);
+                    on[w] = 1;
+                    call.push_back({w, 0});
+                } else if (on[w]) {
+                    low[fr.v] = std::min(low[fr.v], index[w]);
+                }
+            } else {
+                if (low[fr.v] == index[fr.v]) {
+                    std::vector<int> comp;
+                    int w;
+                    do {
+                        w = stack.back();
+                        stack.pop_back();
+                        on[w] = 0;
+                        comp.push_back(w);
+                    } while (w != fr.v);
+                    std::sort(comp.begin(), comp.end());
+                    sccs.push_back(std::move(comp));
+                }
+                const int v = fr.v;
+                call.pop_back();
+                if (!call.empty()) low[call.back().v] = std::min(low[call.back().v], low[v]);
+            }
+        }
+    }
+    return sccs;
+}
+
+struct Fas { std::vector<int> order, lagged; double weight = 0.0; };
+struct Local { std::vector<int> verts; std::vector<std::array<int, 2>> e; std::vector<double> w; std::vector<int> parent; };
+
+static Local induce(int nv, const std::vector<Edge>& edges, const std::vector<int>& vs,
+                    std::vector<int>& scratch) {  // sweepgraph.hpp:156-170
+    Local lg;
+    lg.verts = vs;
+    if ((int)scratch.size() != nv) scratch.assign(nv, -1);
+    for (size_t i = 0; i < vs.size(); ++i) scratch[vs[i]] = (int)i;
+    for (size_t k = 0; k < edges.size(); ++k) {
+        const auto& ed = edges[k];
+        if (scratch[ed.from] >= 0 && scratch[ed.to] >= 0) {
+            lg.e.push_back({scratch[ed.from], scratch[ed.to]});
+            lg.w.push_back(ed.weight);
+            lg.parent.push_back((int)k);
+        }
+    }
+    for (int v : vs) scratch[v] = -1;
+    return lg;
+}
+static Fas order_result(const Local& lg, const std::vector<int>& lo) {  // sweepgraph.hpp:173-186
+    Fas r;
+    std::vector<int> pos(lg.verts.size());
+    for (size_t k = 0; k < lo.size(); ++k) pos[lo[k]] = (int)k;
+    for (size_t k = 0; k < lg.e.size(); ++k)
+        if (pos[lg.e[k][0]] > pos[lg.e[k][1]]) {
+            r.lagged.push_back(lg.parent[k]);
+            r.weight += lg.w[k];
+        }
+    for (int v : lo) r.order.push_back(lg.verts[v]);
+    return r;
+}
+static Fas fas_exact(const Local& lg) {  // sweepgraph.hpp:192-232
+    const int n = (int)lg.verts.size();
+    if (n > 22) throw Error(HSW_ERR_INVALID, "min_fas_exact: component too large");
+    std::vector<double> wout((size_t)n * n, 0.0);
+    for (size_t k = 0; k < lg.e.size(); ++k) wout[(size_t)lg.e[k][0] * n + lg.e[k][1]] += lg.w[k];
+    const uint32_t full = (uint32_t(1) << n) - 1;
+    std::vector<double> dp((size_t)full + 1, std::numeric_limits<double>::infinity());
+    std::vector<int8_t> choice((size_t)full + 1, -1);
+    dp[0] = 0.0;
+    for (uint32_t mask = 1; mask <= full; ++mask)
+        for (int v = 0; v < n; ++v) {
+            if (!(mask & (uint32_t(1) << v))) continue;
+            const uint32_t rest = mask & ~(uint32_t(1) << v);
+            if (dp[rest] == std::numeric_limits<double>::infinity()) continue;
+            double back = 0.0;
+            for (int u = 0; u < n; ++u)
+                if (rest & (uint32_t(1) << u)) back += wout[(size_t)v * n + u];
+            const double cand = dp[rest] + back;
+            if (cand < dp[mask]) {
+                dp[mask] = cand;
+                choice[mask] = (int8_t)v;
+            }
+        }
+    std::vector<int> lo(n);
+    uint32_t mask = full;
+    for (int k = n - 1; k >= 0; --k) {
+        const int v = choice[mask];
+        lo[k] = v;
+        mask &= ~(uint32_t(1) << v);
+    }
+    return order_result(lg, lo);
+}
+static Fas fas_heuristic(const Local& lg) {  // sweepgraph.hpp:238-315
+    const int n = (int)lg.verts.size();
+    std::vector<std::vector<std::pair<int, double>>> out(n), in(n);
+    std::vector<double> wout(n, 0.0), win(n, 0.0);
+    std::vector<int> dout(n, 0), din(n, 0);
+    for (size_t k = 0; k < lg.e.size(); ++k) {
+        const int u = lg.e[k][0], v = lg.e[k][1];
+        const double w = lg.w[k];
+        out[u].push_back({v, w});
+        in[v].push_back({u, w});
+        wout[u] += w;
+        win[v] += w;
+        dout[u]++;
+        din[v]++;
+    }
+    std::vector<char> removed(n, 0);
+    std::vector<int> head, tail;
+    auto drop = [&](int v) {
+        removed[v] = 1;
+        for (const auto& [u, w] : out[v]) {
+            if (removed[u]) continue;
+            din[u]--;
+            win[u] -= w;
+        }
+        for (const auto& [u, w] : in[v]) {
+            if (removed[u]) continue;
+            dout[u]--;
+            wout[u] -= w;
+        }
+    };
+    int left = n;
+    while (left > 0) {
+        bool prog = true;
+        while (prog) {
+            prog = false;
+            for (int v = 0; v < n; ++v)
+                if (!removed[v] && dout[v] == 0) { drop(v); tail.push_back(v); left--; prog = true; }
+        }
+        prog = true;
+        while (prog) {
+            prog = false;
+            for (int v = 0; v < n; ++v)
+                if (!removed[v] && dout[v] > 0 && din[v] == 0) { drop(v); head.push_back(v); left--; prog = true; }
+        }
+        if (left == 0) break;
+        int best = -1;
+        double bd = -std::numeric_limits<double>::infinity();
+        for (int v = 0; v < n; ++v) {
+            if (removed[v]) continue;
+            const double delta = wout[v] - win[v];
+            if (delta > bd) { bd = delta; best = v; }
+        }
+        drop(best);
+        head.push_back(best);
+        left--;
+    }
+    std::vector<int> lo = std::move(head);
+    lo.insert(lo.end(), tail.rbegin(), tail.rend());
+    return order_result(lg, lo);
+}
+
+struct Ordering {
+    std::vector<int> order, position, lagged_edges, level;
+    double lagged_weight = 0.0;
+};
+
+// sweepgraph.hpp:331-396
+static Ordering sweep_ordering(int n, const std::vector<Edge>& edges, int thr) {
+    const auto sccs = tarjan_scc(n, edges);
+    std::vector<int> comp(n, -1);
+    for (size_t c = 0; c < sccs.size(); ++c)
+        for (int v : sccs[c]) comp[v] = (int)c;
+    const int nc = (int)sccs.size();
+    std::vector<std::vector<int>> cout_(nc);
+    std::vector<int> cin(nc, 0);
+    for (const auto& e : edges) {
+        const int cu = comp[e.from], cv = comp[e.to];
+        if (cu != cv) cout_[cu].push_back(cv);
+    }
+    for (int c = 0; c < nc; ++c) {
+        std::sort(cout_[c].begin(), cout_[c].end());
+        cout_[c].erase(std::unique(cout_[c].begin(), cout_[c].end()), cout_[c].end());
+        for (int t : cout_[c]) cin[t]++;
+    }
+    using Key = std::pair<int, int>;
+    std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
+    for (int c = 0; c < nc; ++c)
+        if (cin[c] == 0) ready.push({sccs[c].front(), c});
+    Ordering res;
+    res.order.reserve(n);
+    std::vector<int> scratch;
+    while (!ready.empty()) {
+        const int c = ready.top().second;
+        ready.pop();
+        if (sccs[c].size() == 1) {
+            res.order.push_back(sccs[c].front());
+        } else {
+            const Local lg = induce(n, edges, sccs[c], scratch);
+            const Fas fas = (int)sccs[c].size() <= std::min(thr, 22) ? fas_exact(lg) : fas_heuristic(lg);
+            res.order.insert(res.order.end(), fas.order.begin(), fas.order.end());
+            res.lagged_edges.insert(res.lagged_edges.end(), fas.lagged.begin(), fas.lagged.end());
+            res.lagged_weight += fas.weight;
+        }
+        for (int t : cout_[c])
+            if (--cin[t] == 0) ready.push({sccs[t].front(), t});
+    }
+    if ((int)res.order.size() != n) throw Error(HSW_ERR_LOGIC, "sweep_ordering: condensation was not acyclic");
+    res.position.assign(n, -1);
+    for (int k = 0; k < n; ++k) res.position[res.order[k]] = k;
+    std::vector<char> lag(edges.size(), 0);
+    for (int e : res.lagged_edges) lag[e] = 1;
+    for (size_t e = 0; e < edges.size(); ++e) {
+        const bool backward = res.position[edges[e].from] > res.position[edges[e].to];
+        if (backward != (bool)lag[e]) throw Error(HSW_ERR_LOGIC, "sweep_ordering: retained edge set is inconsistent");
+    }
+    std::sort(res.lagged_edges.begin(), res.lagged_edges.end());
+    return res;
+}
+
+// Small dense LU with partial pivoting (first max on ties); used for the
+// siginvface weights so they are bit-identical to the oracle's.
+static void lu_factor(std::vector<double>& a, std::vector<int>& perm, int n) {
+    perm.resize(n);
+    std::iota(perm.begin(), perm.end(), 0);
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = std::abs(a[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            const double v = std::abs(a[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        if (p != k) {
+            for (int j = 0; j < n; ++j) std::swap(a[(size_t)k * n + j], a[(size_t)p * n + j]);
+            std::swap(perm[k], perm[p]);
+        }
+        const double piv = a[(size_t)k * n + k];
+        if (piv == 0.0) continue;
+        for (int i = k + 1; i < n; ++i) {
+            double& lik = a[(size_t)i * n + k];
+            lik /= piv;
+            const double l = lik;
+            if (l == 0.0) continue;
+            for (int j = k + 1; j < n; ++j) a[(size_t)i * n + j] -= l * a[(size_t)k * n + j];
+        }
+    }
+}
+static void lu_solve(const std::vector<double>& a, const std::vector<int>& perm, int n, const double* b, double* x) {
+    std::vector<double> y(n);
+    for (int i = 0; i < n; ++i) y[i] = b[perm[i]];
+    for (int i = 0; i < n; ++i) {
+        double s = y[i];
+        for (int j = 0; j < i; ++j) s -= a[(size_t)i * n + j] * y[j];
+        y[i] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int j = i + 1; j < n; ++j) s -= a[(size_t)i * n + j] * y[j];
+        y[i] = s / a[(size_t)i * n + i];
+    }
+    for (int i = 0; i < n; ++i) x[i] = y[i];
+}
+
+// =================================================================== setup
+struct Coupling { int face, down, up, down_face, up_face; };
+
+struct Setup {
+    // inputs
+    int dim = 2, p = 1, nb = 4, nfn = 2, nf = 4, nel = 0, nd = 0;
+    Mesh mesh;
+    TensorBasis basis;
+    std::vector<double> ow, odir;  // nd, nd*3
+    std::map<int, std::pair<double, double>> xs;
+    int source_kind = 0;
+    double source_params[8] = {0};
+    double inflow = 0.0;
+    int vol_pts = 0, face_pts = 0, weighting = 1, fas_thr = 10;
+    // quadrature
+    Rule line_v, line_f;
+    std::vector<std::array<double, 3>> vq_pts;
+    std::vector<double> vq_w;
+    std::vector<std::array<double, 2>> fq_pts;
+    std::vector<double> fq_w;
+    int nq = 0, nqf = 0;
+    std::vector<std::vector<int>> fnodes;  // per face, element node ids of face nodes
+    // per element
+    std::vector<double> T;      // E*nb*nb*4
+    std::vector<double> sig_t, sig_s, qvol;  // E, E, E*nb
+    std::vector<double> fgeom;  // E*nf*nqf*4 (normal, w*sj)
+    std::vector<double> fsj;    // E*nf*nqf   (sj)
+    std::vector<int> fnbr;      // E*nf*4
+    std::vector<int> bface_of;  // E*nf -> boundary face id or -1
+    // face trace tables (bit-exact with the reference element-wise arithmetic)
+    std::vector<double> trace;              // nqf * nfn: phi_a at own param point q
+    std::vector<std::vector<double>> traceR;  // per orientation code: nqf * nfn at mapped point
+    // per ordinate
+    std::vector<std::vector<Coupling>> couplings;
+    std::vector<std::vector<double>> weights;
+    std::vector<std::vector<char>> lagged;
+    std::vector<Ordering> ords;
+    std::vector<uint16_t> inflags;  // nd*E
+    // worklists
+    int num_levels = 0;
+    std::vector<int> level_offsets;  // num_levels+1 into pairs_all
+    std::vector<int> pairs_all;      // e*nd + d, sorted (level, e, d)
+    std::vector<std::vector<int>> dir_level_offsets;  // per d
+    std::vector<int> pairs_dir;      // per d block of E pairs sorted by level
+    std::vector<int> face_id_of;     // E*nf -> interior face id or -1
+    std::vector<double> mass_t_cache;  // E*nb*nb for siginvface (exact oracle arithmetic)
+
+    double xs_t(int region) const {
+        auto it = xs.find(region);
+        if (it == xs.end()) it = xs.find(0);
+        if (it == xs.end())
+            throw Error(HSW_ERR_RANGE, "cross sections: no entry for region " + std::to_string(region));
+        return it->second.first;
+    }
+    double xs_s(int region) const {
+        auto it = xs.find(region);
+        if (it == xs.end()) it = xs.find(0);
+        return it->second.second;
+    }
+    double source_at(const double* x) const {
+        if (source_kind == HSW_SOURCE_CONSTANT) return source_params[0];
+        double d2 = 0.0;
+        for (int a = 0; a < dim; ++a) d2 += (x[a] - source_params[a]) * (x[a] - source_params[a]);
+        return d2 < source_params[3] * source_params[3] ? source_params[4] : source_params[5];
+    }
+
+    void ingest(const hsw_problem_desc* D) {
+        if (!D) throw Error(HSW_ERR_INVALID, "hsw_create: null descriptor");
+        if (D->abi_version != HSW_ABI_VERSION) throw Error(HSW_ERR_INVALID, "hsw_create: ABI version mismatch");
+        if (D->dim != 2 && D->dim != 3) throw Error(HSW_ERR_INVALID, "hsw_create: dim must be 2 or 3");
+        if (D->geom_order < 1 || D->geom_order > 8)
+            throw Error(HSW_ERR_INVALID, "hsw_create: geometry order out of range");
+        if (D->basis_order < 1 || (D->dim == 3 && D->basis_order > 4) || D->basis_order > 6)
+            throw Error(HSW_ERR_INVALID, "ReferenceBasis: order out of range for the B200 kernels");
+        if (D->num_elements < 1 || D->num_ordinates < 1 || D->num_ordinates > 4096)
+            throw Error(HSW_ERR_INVALID, "hsw_create: need elements and 1..4096 ordinates");
+        dim = D->dim;
+        p = D->basis_order;
+        mesh.dim = dim;
+        mesh.order = D->geom_order;
+        mesh.geom = TensorBasis(dim, D->geom_order);
+        mesh.npe = mesh.geom.nb;
+        mesh.nel = nel = D->num_elements;
+        mesh.pts.assign(D->points, D->points + (size_t)D->num_points * dim);
+        mesh.enodes.assign(D->element_nodes, D->element_nodes + (size_t)nel * mesh.npe);
+        mesh.region.assign(nel, 1);
+        if (D->element_region) mesh.region.assign(D->element_region, D->element_region + nel);
+        for (int b = 0; b < D->num_boundary_faces; ++b)
+            mesh.bfaces.push_back({D->boundary_faces[3 * b], D->boundary_faces[3 * b + 1], D->boundary_faces[3 * b + 2]});
+        nd = D->num_ordinates;
+        ow.assign(D->ordinate_weight, D->ordinate_weight + nd);
+        odir.assign(D->ordinate_dir, D->ordinate_dir + 3 * nd);
+        for (int r = 0; r < D->num_regions; ++r) {
+            if (!(D->sigma_t[r] >= D->sigma_s[r] && D->sigma_s[r] >= 0.0))
+                throw Error(HSW_ERR_INVALID, "cross sections: need sigma_t >= sigma_s >= 0 (region " +
+                                                 std::to_string(D->region_ids[r]) + ")");
+            xs[D->region_ids[r]] = {D->sigma_t[r], D->sigma_s[r]};
+        }
+        source_kind = D->source_kind;
+        std::memcpy(source_params, D->source_params, sizeof(source_params));
+        inflow = D->inflow;
+        vol_pts = D->volume_points > 0 ? D->volume_points : p + 2;
+        face_pts = D->face_points > 0 ? D->face_points : p + 2;
+        weighting = D->weighting;
+        fas_thr = D->exact_fas_threshold > 0 ? D->exact_fas_threshold : 10;
+        basis = TensorBasis(dim, p);
+        nb = basis.nb;
+        nf = nfaces_of(dim);
+        for (int f = 0; f < nf; ++f) fnodes.push_back(face_nodes(dim, f, p));
+        nfn = (int)fnodes[0].size();
+        if (nfn > kMaxFaceNodes) throw Error(HSW_ERR_INVALID, "hsw_create: too many face nodes");
+        // quadrature rules (quadrature.hpp:93-104 + face Gauss rule)
+        line_v = gauss_legendre(vol_pts);
+        line_f = gauss_legendre(face_pts);
+        if (dim == 2) {
+            for (int j = 0; j < vol_pts; ++j)
+                for (int i = 0; i < vol_pts; ++i) {
+                    vq_pts.push_back({line_v.x[i], line_v.x[j], 0.0});
+                    vq_w.push_back(line_v.w[i] * line_v.w[j]);
+                }
+            for (int i = 0; i < face_pts; ++i) {
+                fq_pts.push_back({line_f.x[i], 0.0});
+                fq_w.push_back(line_f.w[i]);
+            }
+        } else {
+            for (int k = 0; k < vol_pts; ++k)
+                for (int j = 0; j < vol_pts; ++j)
+                    for (int i = 0; i < vol_pts; ++i) {
+                        vq_pts.push_back({line_v.x[i], line_v.x[j], line_v.x[k]});
+                        vq_w.push_back(line_v.w[i] * line_v.w[j] * line_v.w[k]);
+                    }
+            for (int j = 0; j < face_pts; ++j)
+                for (int i = 0; i < face_pts; ++i) {
+                    fq_pts.push_back({line_f.x[i], line_f.x[j]});
+                    fq_w.push_back(line_f.w[i] * line_f.w[j]);
+                }
+        }
+        nq = (int)vq_w.size();
+        nqf = (int)fq_w.size();
+        if (nqf > kMaxFacePoints) throw Error(HSW_ERR_INVALID, "hsw_create: too many face points");
+    }
+
+    void build_mesh(int num_points, bool validate) {
+        mesh.check_connectivity(num_points);
+        mesh.build_faces();
+        face_id_of.assign((size_t)nel * nf, -1);
+        bface_of.assign((size_t)nel * nf, -1);
+        fnbr.assign((size_t)nel * nf * 4, -1);
+        for (size_t i = 0; i < mesh.ifaces.size(); ++i) {
+            const auto& F = mesh.ifaces[i];
+            face_id_of[(size_t)F.el * nf + F.fl] = (int)i;
+            face_id_of[(size_t)F.er * nf + F.fr] = (int)i;
+            int* a = &fnbr[((size_t)F.el * nf + F.fl) * 4];
+            a[0] = F.er; a[1] = F.fr; a[2] = F.orient; a[3] = 0;
+            int* b = &fnbr[((size_t)F.er * nf + F.fr) * 4];
+            b[0] = F.el; b[1] = F.fl; b[2] = orient_inverse(dim, F.orient); b[3] = 1;
+        }
+        for (size_t i = 0; i < mesh.bfaces.size(); ++i) {
+            const auto& B = mesh.bfaces[i];
+            bface_of[(size_t)B.elem * nf + B.face] = (int)i;
+            int* a = &fnbr[((size_t)B.elem * nf + B.face) * 4];
+            a[0] = -1; a[1] = -1; a[2] = 0; a[3] = (int)i;
+        }
+        if (validate) {
+            // mesh.hpp:219-228 det(J) > 0 on an (order+2)^dim lattice
+            const int ns = mesh.order + 2;
+            const int nz = dim == 3 ? ns : 1;
+            std::vector<std::vector<double>> gtab;
+            for (int k = 0; k < nz; ++k)
+                for (int j = 0; j < ns; ++j)
+                    for (int i = 0; i < ns; ++i) {
+                        const double xi[3] = {i / double(ns - 1), j / double(ns - 1), dim == 3 ? k / double(ns - 1) : 0.0};
+                        std::vector<double> g((size_t)mesh.npe * dim);
+                        mesh.geom.gradients(xi, g.data());
+                        gtab.push_back(std::move(g));
+                    }
+            std::atomic<int> bad{std::numeric_limits<int>::max()};
+            parallel_for(nel, [&](int64_t e) {
+                double J[9];
+                for (const auto& g : gtab)
+                    if (mesh.jacobian_tab((int)e, g.data(), J) <= 0.0) {
+                        int cur = bad.load();
+                        while ((int)e < cur && !bad.compare_exchange_weak(cur, (int)e)) {}
+                        return;
+                    }
+            });
+            if (bad.load() != std::numeric_limits<int>::max())
+                throw Error(HSW_ERR_MESH, "mesh: element " + std::to_string(bad.load()) + " has non-positive Jacobian");
+            // mesh.hpp:346-365 trace agreement on a 5-point (5x5) lattice
+            std::vector<double> v((size_t)mesh.npe), vr((size_t)mesh.npe);
+            for (size_t i = 0; i < mesh.ifaces.size(); ++i) {
+                const auto& F = mesh.ifaces[i];
+                const double tol = 1e-12 * mesh.diameter(F.el);
+                const int nt = dim == 3 ? 5 : 1;
+                for (int kt = 0; kt < nt; ++kt)
+                    for (int k = 0; k < 5; ++k) {
+                        const double s = k / 4.0, t = dim == 3 ? kt / 4.0 : 0.0;
+                        double so, to, xil[3], xir[3], xl[3], xr[3];
+                        orient_param(dim, F.orient, s, t, so, to);
+                        param_point(dim, F.fl, s, t, xil);
+                        param_point(dim, F.fr, so, to, xir);
+                        mesh.geom.values(xil, v.data());
+                        mesh.geom.values(xir, vr.data());
+                        mesh.map_tab(F.el, v.data(), xl);
+                        mesh.map_tab(F.er, vr.data(), xr);
+                        double d2 = 0.0;
+                        for (int a = 0; a < dim; ++a) d2 += (xl[a] - xr[a]) * (xl[a] - xr[a]);
+                        if (std::sqrt(d2) > tol)
+                            throw Error(HSW_ERR_MESH, "mesh: interior face " + std::to_string(i) +
+                                                          " traces disagree between elements " +
+                                                          std::to_string(F.el) + " and " + std::to_string(F.er));
+                    }
+            }
+        }
+    }
+
+    // assembly.hpp:58-93 + 143-163 + 278-300: per element M, G_k, volume source
+    void element_tensors() {
+        // basis tables at the volume points (element independent)
+        std::vector<double> U((size_t)nq * nb), DU((size_t)nq * nb * dim);
+        std::vector<double> GV((size_t)nq * mesh.npe), GG((size_t)nq * mesh.npe * dim);
+        for (int q = 0; q < nq; ++q) {
+            basis.values(vq_pts[q].data(), &U[(size_t)q * nb]);
+            basis.gradients(vq_pts[q].data(), &DU[(size_t)q * nb * dim]);
+            mesh.geom.values(vq_pts[q].data(), &GV[(size_t)q * mesh.npe]);
+            mesh.geom.gradients(vq_pts[q].data(), &GG[(size_t)q * mesh.npe * dim]);
+        }
+        T.assign((size_t)nel * nb * nb * 4, 0.0);
+        sig_t.resize(nel);
+        sig_s.resize(nel);
+        qvol.assign((size_t)nel * nb, 0.0);
+        if (weighting == HSW_WEIGHT_SIGINVFACE) mass_t_cache.assign((size_t)nel * nb * nb, 0.0);
+        parallel_for(nel, [&](int64_t e64) {
+            const int e = (int)e64;
+            const double st = xs_t(mesh.region[e]);
+            sig_t[e] = st;
+            sig_s[e] = xs_s(mesh.region[e]);
+            std::vector<double> W((size_t)(dim + 1) * nq * nb);
+            std::vector<double> wdet(nq);
+            for (int q = 0; q < nq; ++q) {
+                double J[9], K[9], x[3];
+                const double det = mesh.jacobian_tab(e, &GG[(size_t)q * mesh.npe * dim], J);
+                if (det <= 0.0 || !std::isfinite(det))
+                    throw Error(HSW_ERR_ASSEMBLY, "assembly: singular Jacobian in element " + std::to_string(e));
+                mesh.inverse(J, K);
+                const double wd = vq_w[q] * det;
+                wdet[q] = wd;
+                const double* du = &DU[(size_t)q * nb * dim];
+                for (int m = 0; m < nb; ++m) {
+                    W[((size_t)0 * nq + q) * nb + m] = U[(size_t)q * nb + m] * wd;
+                    for (int k = 0; k < dim; ++k) {
+                        double v = 0.0;
+                        for (int j = 0; j < dim; ++j) v += K[j * 3 + k] * du[m * dim + j];
+                        W[((size_t)(k + 1) * nq + q) * nb + m] = v * wd;
+                    }
+                }
+                mesh.map_tab(e, &GV[(size_t)q * mesh.npe], x);
+                const double s = vq_w[q] * det * source_at(x);  // assembly.hpp:298
+                for (int m = 0; m < nb; ++m) qvol[(size_t)e * nb + m] += s * U[(size_t)q * nb + m];
+            }
+            std::vector<double> acc((size_t)nb);
+            double* Te = &T[(size_t)e * nb * nb * 4];
+            for (int k = 0; k <= dim; ++k) {
+                const double sign = k == 0 ? 1.0 : -1.0;
+                for (int m = 0; m < nb; ++m) {
+                    std::fill(acc.begin(), acc.end(), 0.0);
+                    for (int q = 0; q < nq; ++q) {
+                        const double w = W[((size_t)k * nq + q) * nb + m];
+                        const double* u = &U[(size_t)q * nb];
+                        for (int n = 0; n < nb; ++n) acc[n] += w * u[n];
+                    }
+                    for (int n = 0; n < nb; ++n) Te[((size_t)m * nb + n) * 4 + k] = sign * acc[n];
+                }
+            }
+            if (!mass_t_cache.empty()) {  // exact reference M_t arithmetic (assembly.hpp:157-158)
+                double* mt = &mass_t_cache[(size_t)e * nb * nb];
+                for (int m = 0; m < nb; ++m)
+                    for (int n = 0; n < nb; ++n) {
+                        double s = 0.0;
+                        for (int q = 0; q < nq; ++q)
+                            s += U[(size_t)q * nb + m] * (wdet[q] * st) * U[(size_t)q * nb + n];
+                        mt[(size_t)m * nb + n] = s;
+                    }
+            }
+        });
+    }
+
+    // per element face geometry (own side) + trace tables
+    void face_tables() {
+        std::vector<std::vector<double>> GGf(nf);  // per face: nqf * npe * dim gradient tables
+        for (int f = 0; f < nf; ++f) {
+            GGf[f].resize((size_t)nqf * mesh.npe * dim);
+            for (int q = 0; q < nqf; ++q) {
+                double xi[3];
+                param_point(dim, f, fq_pts[q][0], fq_pts[q][1], xi);
+                mesh.geom.gradients(xi, &GGf[f][(size_t)q * mesh.npe * dim]);
+            }
+        }
+        fgeom.assign((size_t)nel * nf * nqf * 4, 0.0);
+        fsj.assign((size_t)nel * nf * nqf, 0.0);
+        parallel_for(nel, [&](int64_t e64) {
+            const int e = (int)e64;
+            for (int f = 0; f < nf; ++f)
+                for (int q = 0; q < nqf; ++q) {
+                    double n[3], sj;
+                    mesh.face_geometry_tab(e, f, &GGf[f][(size_t)q * mesh.npe * dim], n, sj);
+                    double* g = &fgeom[(((size_t)e * nf + f) * nqf + q) * 4];
+                    g[0] = n[0]; g[1] = n[1]; g[2] = n[2];
+                    g[3] = fq_w[q] * sj;
+                    fsj[((size_t)e * nf + f) * nqf + q] = sj;
+                }
+        });
+        // traces: full basis values at the face param point, face nodes picked
+        // (assembly.hpp:112-116); identical for every face (one factor is exactly 1).
+        std::vector<double> full(nb);
+        trace.assign((size_t)nqf * nfn, 0.0);
+        for (int q = 0; q < nqf; ++q) {
+            double xi[3];
+            param_point(dim, 0, fq_pts[q][0], fq_pts[q][1], xi);
+            basis.values(xi, full.data());
+            for (int a = 0; a < nfn; ++a) trace[(size_t)q * nfn + a] = full[fnodes[0][a]];
+        }
+        const int ncodes = dim == 2 ? 2 : 8;
+        traceR.assign(ncodes, std::vector<double>((size_t)nqf * nfn, 0.0));
+        for (int c = 0; c < ncodes; ++c)
+            for (int q = 0; q < nqf; ++q) {
+                double so, to, xi[3];
+                orient_param(dim, c, fq_pts[q][0], fq_pts[q][1], so, to);
+                param_point(dim, 0, so, to, xi);
+                basis.values(xi, full.data());
+                for (int a = 0; a < nfn; ++a) traceR[c][(size_t)q * nfn + a] = full[fnodes[0][a]];
+            }
+    }
+
+    // assembly.hpp:185-241 (interior faces, Gauss rule) -> couplings + weights,
+    // then sweepgraph.hpp:54-77 + 331-396, lag flags (solver.hpp:63-66) and levels.
+    void ordinates() {
+        couplings.assign(nd, {});
+        weights.assign(nd, {});
+        lagged.assign(nd, {});
+        ords.assign(nd, {});
+        inflags.assign((size_t)nd * nel, 0);
+        const int nfi = (int)mesh.ifaces.size();
+        parallel_for(nd, [&](int64_t d64) {
+            const int d = (int)d64;
+            const double* om = &odir[3 * d];
+            std::vector<double> LR((size_t)nfn * nfn), RL((size_t)nfn * nfn), wp(nqf), wm(nqf);
+            auto& cpl = couplings[d];
+            auto& wts = weights[d];
+            for (int fi = 0; fi < nfi; ++fi) {
+                const IFace& F = mesh.ifaces[fi];
+                const double* geo = &fgeom[(((size_t)F.el * nf + F.fl) * nqf) * 4];
+                const double* sjv = &fsj[((size_t)F.el * nf + F.fl) * nqf];
+                std::fill(LR.begin(), LR.end(), 0.0);
+                std::fill(RL.begin(), RL.end(), 0.0);
+                double length = 0.0;
+                const double* uR0 = traceR[F.orient].data();
+                for (int q = 0; q < nqf; ++q) {
+                    double on = 0.0;
+                    for (int k = 0; k < dim; ++k) on += om[k] * geo[q * 4 + k];
+                    const double wplus = 0.5 * (on + std::abs(on));
+                    const double wminus = 0.5 * (std::abs(on) - on);
+                    const double sj = sjv[q], w = fq_w[q];
+                    const double* ul = &trace[(size_t)q * nfn];
+                    const double* ur = &uR0[(size_t)q * nfn];
+                    if (wminus != 0.0)
+                        for (int m = 0; m < nfn; ++m) {
+                            const double c = wminus * ul[m];
+                            double* row = &LR[(size_t)m * nfn];
+                            for (int n = 0; n < nfn; ++n) row[n] += w * (c * ur[n] * sj);
+                        }
+                    if (wplus != 0.0)
+                        for (int m = 0; m < nfn; ++m) {
+                            const double c = wplus * ur[m];
+                            double* row = &RL[(size_t)m * nfn];
+                            for (int n = 0; n < nfn; ++n) row[n] += w * (c * ul[n] * sj);
+                        }
+                    length += w * sj;
+                }
+                const double eps = 1e-12 * length;
+                double mlr = 0.0, mrl = 0.0;
+                for (size_t k = 0; k < LR.size(); ++k) {
+                    mlr = std::max(mlr, std::abs(LR[k]));
+                    mrl = std::max(mrl, std::abs(RL[k]));
+                }
+                if (mlr > eps) {
+                    cpl.push_back({fi, F.el, F.er, F.fl, F.fr});
+                    wts.push_back(weight_of(mlr, F.el, F.fl, LR, false));
+                }
+                if (mrl > eps) {
+                    cpl.push_back({fi, F.er, F.el, F.fr, F.fl});
+                    wts.push_back(weight_of(mrl, F.er, F.fr, RL, false));
+                }
+            }
+            std::vector<Edge> edges(cpl.size());
+            for (size_t c = 0; c < cpl.size(); ++c) edges[c] = {cpl[c].up, cpl[c].down, wts[c]};
+            ords[d] = sweep_ordering(nel, edges, fas_thr);
+            Ordering& o = ords[d];
+            auto& lg = lagged[d];
+            lg.assign(cpl.size(), 0);
+            std::vector<std::vector<int>> incoming(nel);
+            for (size_t c = 0; c < cpl.size(); ++c) {
+                lg[c] = o.position[cpl[c].up] > o.position[cpl[c].down];
+                incoming[cpl[c].down].push_back((int)c);
+                uint16_t& fl = inflags[(size_t)d * nel + cpl[c].down];
+                fl |= (uint16_t)(1u << (2 * cpl[c].down_face));
+                if (lg[c]) fl |= (uint16_t)(1u << (2 * cpl[c].down_face + 1));
+            }
+            o.level.assign(nel, 0);
+            for (int e : o.order) {
+                int lv = 0;
+                for (int c : incoming[e])
+                    if (!lg[c]) lv = std::max(lv, o.level[cpl[c].up] + 1);
+                o.level[e] = lv;
+            }
+        });
+    }
+
+    // face -> max|block|; siginvface -> max|M_t^{-1} block| (sweepgraph.hpp:60-72)
+    double weight_of(double maxabs, int down, int down_face, const std::vector<double>& blk, bool) const {
+        if (weighting == HSW_WEIGHT_UNITY) return 1.0;
+        if (weighting == HSW_WEIGHT_FACE) return maxabs;
+        std::vector<double> a(mass_t_cache.begin() + (size_t)down * nb * nb,
+                              mass_t_cache.begin() + (size_t)(down + 1) * nb * nb);
+        std::vector<int> perm;
+        lu_factor(a, perm, nb);
+        double w = 0.0;
+        std::vector<double> col(nb), x(nb);
+        for (int n = 0; n < nfn; ++n) {
+            std::fill(col.begin(), col.end(), 0.0);
+            for (int m = 0; m < nfn; ++m) col[fnodes[down_face][m]] = -blk[(size_t)m * nfn + n];
+            lu_solve(a, perm, nb, col.data(), x.data());
+            for (int i = 0; i < nb; ++i) {
+                if (!std::isfinite(x[i]))
+                    throw Error(HSW_ERR_ASSEMBLY, "sig_inv_face weighting: singular mass matrix on element " +
+                                                      std::to_string(down));
+                w = std::max(w, std::abs(x[i]));
+            }
+        }
+        return w;
+    }
+
+    void worklists() {
+        int maxl = 0;
+        for (int d = 0; d < nd; ++d)
+            for (int e = 0; e < nel; ++e) maxl = std::max(maxl, ords[d].level[e]);
+        num_levels = maxl + 1;
+        // all-ordinate worklist sorted by (level, element, ordinate)
+        std::vector<int> count(num_levels + 1, 0);
+        for (int e = 0; e < nel; ++e)
+            for (int d = 0; d < nd; ++d) count[ords[d].level[e] + 1]++;
+        for (int l = 0; l < num_levels; ++l) count[l + 1] += count[l];
+        level_offsets = count;
+        pairs_all.assign((size_t)nel * nd, 0);
+        std::vector<int> fill(count.begin(), count.end() - 1);
+        for (int e = 0; e < nel; ++e)
+            for (int d = 0; d < nd; ++d) pairs_all[fill[ords[d].level[e]]++] = e * nd + d;
+        // per-ordinate worklists
+        pairs_dir.assign((size_t)nel * nd, 0);
+        dir_level_offsets.assign(nd, {});
+        for (int d = 0; d < nd; ++d) {
+            int ml = 0;
+            for (int e = 0; e < nel; ++e) ml = std::max(ml, ords[d].level[e]);
+            std::vector<int> c(ml + 2, 0);
+            for (int e = 0; e < nel; ++e) c[ords[d].level[e] + 1]++;
+            for (int l = 0; l <= ml; ++l) c[l + 1] += c[l];
+            dir_level_offsets[d] = c;
+            std::vector<int> fl(c.begin(), c.end() - 1);
+            int* base = &pairs_dir[(size_t)d * nel];
+            for (int e = 0; e < nel; ++e) base[fl[ords[d].level[e]]++] = e * nd + d;
+        }
+    }
+};
+
+}  // namespace hsw
+
+// ===================================================================== C ABI
+using namespace hsw;
+
+struct hsw_handle {
+    Setup S;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevProblem P{};
+    // device buffers
+    double *d_T = nullptr, *d_sig_t = nullptr, *d_sig_s = nullptr, *d_qvol = nullptr, *d_fgeom = nullptr;
+    int* d_fnbr = nullptr;
+    uint16_t* d_inflags = nullptr;
+    double *d_omega = nullptr, *d_weight = nullptr;
+    double *d_psiA = nullptr, *d_psiB = nullptr, *d_phi = nullptr, *d_phi_old = nullptr, *d_src = nullptr;
+    double *d_scratch = nullptr, *d_out = nullptr, *d_vec = nullptr, *d_vec2 = nullptr;
+    int *d_pairs_all = nullptr, *d_pairs_dir = nullptr;
+    unsigned long long* d_err = nullptr;
+    double* h_out = nullptr;  // pinned
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t zero_pair = -1;
+    int64_t last_launches = 0;
+    double last_kernel_ms = 0.0;
+    size_t N = 0;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+#define CUDA_OK(x)                                                                           \
+    do {                                                                                     \
+        cudaError_t _e = (x);                                                                \
+        if (_e != cudaSuccess)                                                               \
+            throw hsw::Error(HSW_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(_e) + \
+                                               " at " #x);                                   \
+    } while (0)
+
+template <typename T>
+T* dev_upload(const std::vector<T>& v) {
+    T* p = nullptr;
+    if (v.empty()) return nullptr;
+    CUDA_OK(cudaMalloc(&p, v.size() * sizeof(T)));
+    CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+}
+
+void free_handle(hsw_handle* h) {
+    if (!h) return;
+    void* bufs[] = {h->d_T, h->d_sig_t, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
+                    h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
+                    h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_err};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (h->h_out) cudaFreeHost(h->h_out);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+void need_device(const hsw_handle* h) {
+    if (!h || !h->stream)
+        throw hsw::Error(HSW_ERR_CUDA, "handle has no device state (created with device < 0); "
+                                       "the B200 sweep has no CPU fallback");
+}
+
+// Raise the first singular (element, ordinate) recorded by the kernels.
+void check_err(hsw_handle* h) {
+    unsigned long long key = 0;
+    CUDA_OK(cudaMemcpyAsync(&key, h->d_err, sizeof(key), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    if (key != ~0ull) {
+        const int nd = h->S.nd;
+        const long long pr = (long long)(key & 0xffffffffffull);
+        const int e = (int)(pr / nd), d = (int)(pr % nd);
+        const unsigned long long reset = ~0ull;
+        CUDA_OK(cudaMemcpy(h->d_err, &reset, sizeof(reset), cudaMemcpyHostToDevice));
+        throw hsw::Error(HSW_ERR_SOLVER, "local streaming+collision block is singular (element " +
+                                             std::to_string(e) + ", ordinate " + std::to_string(d) + ")");
+    }
+}
+
+// All-ordinate sweep psi_old -> psi_new using the current h->d_src.
+void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
+    const auto& off = h->S.level_offsets;
+    if (time_it) CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launches = 0;
+    for (int l = 0; l < h->S.num_levels; ++l) {
+        const int n = off[l + 1] - off[l];
+        if (n == 0) continue;
+        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, h->d_pairs_all + off[l], n, h->d_err, h->zero_pair,
+                        h->stream);
+        ++launches;
+    }
+    if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+    h->last_launches = launches;
+}
+
+void run_dir_levels(hsw_handle* h, int d, const double* psi_old, double* psi_new) {
+    const auto& off = h->S.dir_level_offsets[d];
+    const int* base = h->d_pairs_dir + (size_t)d * h->S.nel;
+    for (size_t l = 0; l + 1 < off.size(); ++l) {
+        const int n = off[l + 1] - off[l];
+        if (n == 0) continue;
+        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, base + off[l], n, h->d_err, h->zero_pair, h->stream);
+    }
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const hsw::Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(HSW_ERR_NOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(HSW_ERR_INVALID, e.what());
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int hsw_last_error(char* buf, size_t len) {
+    if (buf && len) std::snprintf(buf, len, "%s", g_last_error.c_str());
+    return (int)g_last_error.size();
+}
+
+int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
+    if (!out) return fail(HSW_ERR_INVALID, "hsw_create: null output handle");
+    *out = nullptr;
+    hsw_handle* h = new hsw_handle();
+    const int rc = guarded([&] {
+        Setup& S = h->S;
+        S.ingest(desc);
+        S.build_mesh(desc->num_points, desc->validate_geometry != 0);
+        S.element_tensors();
+        S.face_tables();
+        S.ordinates();
+        S.worklists();
+        // device (device < 0: host-only plan, used by the CPU tests of the host logic)
+        if (desc->device < 0) return HSW_OK;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw hsw::Error(HSW_ERR_CUDA, "hsw_create: no CUDA device available (the B200 sweep has no CPU fallback)");
+        h->device = desc->device;
+        CUDA_OK(cudaSetDevice(h->device));
+        CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreate(&h->ev0));
+        CUDA_OK(cudaEventCreate(&h->ev1));
+        ConstTables ct{};
+        for (int f = 0; f < S.nf; ++f)
+            for (int a = 0; a < S.nfn; ++a) ct.fnode[f][a] = S.fnodes[f][a];
+        for (int q = 0; q < S.nqf; ++q)
+            for (int a = 0; a < S.nfn; ++a) ct.trace[q][a] = S.trace[(size_t)q * S.nfn + a];
+        dev_upload_tables(ct);
+        h->d_T = dev_upload(S.T);
+        h->d_sig_t = dev_upload(S.sig_t);
+        h->d_sig_s = dev_upload(S.sig_s);
+        h->d_qvol = dev_upload(S.qvol);
+        h->d_fgeom = dev_upload(S.fgeom);
+        h->d_fnbr = dev_upload(S.fnbr);
+        h->d_inflags = dev_upload(S.inflags);
+        std::vector<double> om((size_t)S.nd * 4, 0.0);
+        for (int d = 0; d < S.nd; ++d)
+            for (int k = 0; k < 3; ++k) om[(size_t)d * 4 + k] = k < S.dim ? S.odir[3 * d + k] : 0.0;
+        h->d_omega = dev_upload(om);
+        h->d_weight = dev_upload(S.ow);
+        h->d_pairs_all = dev_upload(S.pairs_all);
+        h->d_pairs_dir = dev_upload(S.pairs_dir);
+        h->N = (size_t)S.nel * S.nb;
+        const size_t psi_bytes = h->N * S.nd * sizeof(double);
+        CUDA_OK(cudaMalloc(&h->d_psiA, psi_bytes));
+        CUDA_OK(cudaMalloc(&h->d_psiB, psi_bytes));
+        CUDA_OK(cudaMemset(h->d_psiA, 0, psi_bytes));
+        CUDA_OK(cudaMemset(h->d_psiB, 0, psi_bytes));
+        CUDA_OK(cudaMalloc(&h->d_phi, h->N * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_phi_old, h->N * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_src, h->N * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_vec, h->N * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_vec2, h->N * sizeof(double)));
+        CUDA_OK(cudaMemset(h->d_phi, 0, h->N * sizeof(double)));
+        CUDA_OK(cudaMemset(h->d_phi_old, 0, h->N * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_scratch, (size_t)3 * 65536 * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_out, 8 * sizeof(double)));
+        CUDA_OK(cudaMalloc(&h->d_err, sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
+        CUDA_OK(cudaMallocHost(&h->h_out, 8 * sizeof(double)));
+        DevProblem& P = h->P;
+        P.dim = S.dim; P.p = S.p; P.nb = S.nb; P.nfn = S.nfn; P.nqf = S.nqf; P.nfaces = S.nf;
+        P.nel = S.nel; P.nd = S.nd;
+        P.T = h->d_T; P.sig_t = h->d_sig_t; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
+        P.fgeom = h->d_fgeom; P.fnbr = h->d_fnbr; P.inflags = h->d_inflags;
+        P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;
+        if (desc->check_local_blocks) {
+            // SweepSolver ctor factor check (solver.hpp:67-75): one sweep on zero data
+            dev_scatter_source(P, h->d_phi, h->d_src, h->stream);
+            run_all_levels(h, h->d_psiA, h->d_psiB, false);
+            check_err(h);
+        }
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        return HSW_OK;
+    });
+    if (rc != HSW_OK) {
+        free_handle(h);
+        return rc;
+    }
+    *out = h;
+    return HSW_OK;
+}
+
+void hsw_destroy(hsw_handle* h) { free_handle(h); }
+
+int hsw_sizes(const hsw_handle* h, int64_t out[6]) {
+    if (!h || !out) return fail(HSW_ERR_INVALID, "hsw_sizes: null argument");
+    out[0] = h->S.nel;
+    out[1] = h->S.nb;
+    out[2] = h->S.nd;
+    out[3] = (int64_t)h->N;
+    out[4] = (int64_t)h->S.mesh.ifaces.size();
+    out[5] = h->S.num_levels;
+    return HSW_OK;
+}
+
+int hsw_ordering(const hsw_handle* h, int d, int* order, int* position, int* lagged, int lagged_cap,
+                 int* num_lagged, double* lagged_weight, int* level) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_ordering: null handle");
+    if (d < 0 || d >= h->S.nd) return fail(HSW_ERR_RANGE, "vector::_M_range_check: ordinate " + std::to_string(d));
+    const Ordering& o = h->S.ords[d];
+    if (order) std::copy(o.order.begin(), o.order.end(), order);
+    if (position) std::copy(o.position.begin(), o.position.end(), position);
+    if (level) std::copy(o.level.begin(), o.level.end(), level);
+    if (lagged) std::copy(o.lagged_edges.begin(), o.lagged_edges.begin() + std::min<size_t>(lagged_cap, o.lagged_edges.size()), lagged);
+    if (num_lagged) *num_lagged = (int)o.lagged_edges.size();
+    if (lagged_weight) *lagged_weight = o.lagged_weight;
+    return HSW_OK;
+}
+
+int hsw_total_lagged_edges(const hsw_handle* h, int64_t* out) {
+    if (!h || !out) return fail(HSW_ERR_INVALID, "hsw_total_lagged_edges: null argument");
+    int64_t n = 0;
+    for (const auto& o : h->S.ords) n += (int64_t)o.lagged_edges.size();
+    *out = n;
+    return HSW_OK;
+}
+
+int hsw_couplings(const hsw_handle* h, int d, int* ints4, double* weights, int cap, int* count) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_couplings: null handle");
+    if (d < 0 || d >= h->S.nd) return fail(HSW_ERR_RANGE, "hsw_couplings: ordinate out of range");
+    const auto& c = h->S.couplings[d];
+    if (count) *count = (int)c.size();
+    const int n = std::min<int>(cap, (int)c.size());
+    for (int i = 0; i < n; ++i) {
+        if (ints4) {
+            ints4[4 * i] = c[i].face;
+            ints4[4 * i + 1] = c[i].down;
+            ints4[4 * i + 2] = c[i].up;
+            ints4[4 * i + 3] = h->S.lagged[d][i];
+        }
+        if (weights) weights[i] = h->S.weights[d][i];
+    }
+    return HSW_OK;
+}
+
+int hsw_interior_faces(const hsw_handle* h, int* ints5, int cap, int* count) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_interior_faces: null handle");
+    const auto& f = h->S.mesh.ifaces;
+    if (count) *count = (int)f.size();
+    const int n = std::min<int>(cap, (int)f.size());
+    for (int i = 0; i < n && ints5; ++i) {
+        ints5[5 * i] = f[i].el; ints5[5 * i + 1] = f[i].er; ints5[5 * i + 2] = f[i].fl;
+        ints5[5 * i + 3] = f[i].fr; ints5[5 * i + 4] = f[i].orient;
+    }
+    return HSW_OK;
+}
+
+int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out) {
+    return guarded([&] {
+        if (!h || !rhs || !out) throw hsw::Error(HSW_ERR_INVALID, "hsw_local_solve: null argument");
+        need_device(h);
+        if (e < 0 || e >= h->S.nel || d < 0 || d >= h->S.nd)
+            throw hsw::Error(HSW_ERR_RANGE, "hsw_local_solve: element/ordinate out of range");
+        const size_t nb = h->S.nb;
+        CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        dev_local_solve(h->P, e, d, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        CUDA_OK(cudaMemcpyAsync(out, h->d_vec2, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        check_err(h);
+        return HSW_OK;
+    });
+}
+
+int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* psi_old_dev, double* psi_new_dev) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep_device: null handle");
+        need_device(h);
+        if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
+        dev_scatter_source(h->P, phi_dev, h->d_src, h->stream);
+        if (d == -1) {
+            run_all_levels(h, psi_old_dev, psi_new_dev, false);
+        } else {
+            // single-ordinate vectors: shift the base so slot d addresses them
+            const double* po = psi_old_dev - (ptrdiff_t)d * (ptrdiff_t)h->N;
+            double* pn = psi_new_dev - (ptrdiff_t)d * (ptrdiff_t)h->N;
+            run_dir_levels(h, d, po, pn);
+        }
+        return HSW_OK;
+    });
+}
+
+int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, double* psi_new) {
+    return guarded([&] {
+        if (!h || !phi || !psi_old || !psi_new) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep: null argument");
+        need_device(h);
+        if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
+        const size_t N = h->N;
+        CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        if (d == -1) {
+            CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi_old, N * h->S.nd * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+            run_all_levels(h, h->d_psiA, h->d_psiB, false);
+            CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB, N * h->S.nd * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        } else {
+            double* slotA = h->d_psiA + (size_t)d * N;
+            double* slotB = h->d_psiB + (size_t)d * N;
+            CUDA_OK(cudaMemcpyAsync(slotA, psi_old, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+            run_dir_levels(h, d, h->d_psiA, h->d_psiB);
+            CUDA_OK(cudaMemcpyAsync(psi_new, slotB, N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        }
+        check_err(h);
+        return HSW_OK;
+    });
+}
+
+int hsw_direct_oracle(hsw_handle* h, int d, const double* phi, double* psi) {
+    return guarded([&] {
+        if (!h || !phi || !psi) throw hsw::Error(HSW_ERR_INVALID, "hsw_direct_oracle: null argument");
+        need_device(h);
+        if (d < 0 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_direct_oracle: ordinate out of range");
+        const size_t N = h->N;
+        double* slotA = h->d_psiA + (size_t)d * N;
+        double* slotB = h->d_psiB + (size_t)d * N;
+        CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CUDA_OK(cudaMemsetAsync(slotA, 0, N * sizeof(double), h->stream));
+        dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+        double prev = INFINITY;
+        for (int it = 0; it < 2000; ++it) {
+            run_dir_levels(h, d, h->d_psiA, h->d_psiB);
+            dev_max_abs_diff(slotA, slotB, (int64_t)N, h->d_scratch, h->d_out, h->stream);
+            CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CUDA_OK(cudaMemcpyAsync(slotA, slotB, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+            check_err(h);
+            const double diff = h->h_out[0];
+            if (h->S.ords[d].lagged_edges.empty() || diff == 0.0 || (diff >= prev && it > 3)) break;
+            prev = diff;
+        }
+        CUDA_OK(cudaMemcpyAsync(psi, slotB, N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        return HSW_OK;
+    });
+}
+
+int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_result* res, double* psi_out,
+                         double* phi_out, double* err_hist, double* phi_hist) {
+    return guarded([&] {
+        if (!h || !opts) throw hsw::Error(HSW_ERR_INVALID, "hsw_source_iteration: null argument");
+        need_device(h);
+        const size_t N = h->N;
+        const int nd = h->S.nd;
+        CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
+        CUDA_OK(cudaMemsetAsync(h->d_phi, 0, N * sizeof(double), h->stream));
+        double* cur = h->d_psiA;
+        double* nxt = h->d_psiB;
+        double* phi_cur = h->d_phi;
+        double* phi_nxt = h->d_phi_old;
+        hsw_si_result r{};
+        cudaEvent_t t0, t1;
+        CUDA_OK(cudaEventCreate(&t0));
+        CUDA_OK(cudaEventCreate(&t1));
+        CUDA_OK(cudaEventRecord(t0, h->stream));
+        for (int it = 0; it < opts->max_iterations; ++it) {
+            dev_scatter_source(h->P, phi_cur, h->d_src, h->stream);
+            if (opts->mode == HSW_MODE_DIRECT) {
+                // direct_oracle per ordinate with phi fixed (solver.hpp:145-149)
+                for (int d = 0; d < nd; ++d) {
+                    double* a = cur + (size_t)d * N;
+                    double* b = nxt + (size_t)d * N;
+                    CUDA_OK(cudaMemcpyAsync(h->d_vec, a, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                    for (int k = 0; k < 2000; ++k) {
+                        // iterate on slot d of cur using a scratch copy so cur keeps psi_old
+                        run_dir_levels(h, d, h->d_vec - (ptrdiff_t)d * (ptrdiff_t)N, nxt);
+                        dev_max_abs_diff(h->d_vec, b, (int64_t)N, h->d_scratch, h->d_out, h->stream);
+                        CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+                        CUDA_OK(cudaMemcpyAsync(h->d_vec, b, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                        CUDA_OK(cudaStreamSynchronize(h->stream));
+                        if (h->S.ords[d].lagged_edges.empty() || h->h_out[0] == 0.0 || k > 200) break;
+                    }
+                }
+            } else {
+                run_all_levels(h, cur, nxt, false);
+            }
+            dev_phi_and_norms(h->P, nxt, cur, phi_cur, phi_nxt, h->d_scratch, h->d_out, h->stream);
+            CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            check_err(h);
+            const double err = h->h_out[0];
+            const double num = h->h_out[1], den = h->h_out[2];
+            const double rel = den > 0.0 ? std::sqrt(num) / std::sqrt(den) : (num > 0.0 ? INFINITY : 0.0);
+            if (err_hist) err_hist[it] = err;
+            if (phi_hist) phi_hist[it] = rel;
+            std::swap(cur, nxt);
+            std::swap(phi_cur, phi_nxt);
+            r.iterations = it + 1;
+            r.final_error = err;
+            r.final_phi_rel = rel;
+            const double crit = opts->criterion == HSW_CRIT_PSI_LINF ? err : rel;
+            if (crit < opts->tolerance) {
+                r.converged = 1;
+                break;
+            }
+        }
+        CUDA_OK(cudaEventRecord(t1, h->stream));
+        CUDA_OK(cudaEventSynchronize(t1));
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, t0, t1));
+        r.seconds = ms * 1e-3;
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        if (psi_out) CUDA_OK(cudaMemcpyAsync(psi_out, cur, N * nd * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        if (phi_out) CUDA_OK(cudaMemcpyAsync(phi_out, phi_cur, N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        // keep the converged state in psiA / phi for hsw_device_state
+        if (cur != h->d_psiA) std::swap(h->d_psiA, h->d_psiB);
+        if (phi_cur != h->d_phi) std::swap(h->d_phi, h->d_phi_old);
+        if (res) *res = r;
+        return HSW_OK;
+    });
+}
+
+int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5[5], int* attrs, double* vals,
+                int cap, int* count) {
+    return guarded([&] {
+        if (!h || !psi || !phi || !out5) throw hsw::Error(HSW_ERR_INVALID, "hsw_balance: null argument");
+        const Setup& S = h->S;
+        const size_t N = h->N;
+        const int nfn = S.nfn, nqf = S.nqf, nb = S.nb;
+        double sv = 0.0, inflow_tot = 0.0, absorption = 0.0, outflow = 0.0;
+        std::map<int, double> by_attr;
+        double qsum = 0.0;
+        for (size_t i = 0; i < N; ++i) qsum += S.qvol[i];
+        for (int d = 0; d < S.nd; ++d) {
+            const double w = S.ow[d];
+            const double* om = &S.odir[3 * d];
+            sv += w * qsum;
+            double inf_d = 0.0;
+            for (size_t bi = 0; bi < S.mesh.bfaces.size(); ++bi) {
+                const auto& B = S.mesh.bfaces[bi];
+                const double* geo = &S.fgeom[(((size_t)B.elem * S.nf + B.face) * nqf) * 4];
+                const double* psie = psi + (size_t)d * N + (size_t)B.elem * nb;
+                double o = 0.0;
+                for (int q = 0; q < nqf; ++q) {
+                    double on = 0.0;
+                    for (int k = 0; k < S.dim; ++k) on += om[k] * geo[q * 4 + k];
+                    const double wplus = 0.5 * (on + std::abs(on));
+                    const double wminus = 0.5 * (std::abs(on) - on);
+                    double tr = 0.0, ts = 0.0;
+                    for (int a = 0; a < nfn; ++a) {
+                        tr += S.trace[(size_t)q * nfn + a] * psie[S.fnodes[B.face][a]];
+                        ts += S.trace[(size_t)q * nfn + a];
+                    }
+                    o += geo[q * 4 + 3] * wplus * tr * ts;
+                    inf_d += geo[q * 4 + 3] * wminus * S.inflow * ts;
+                }
+                o *= w;
+                outflow += o;
+                by_attr[B.attr] += o;
+            }
+            inflow_tot += w * inf_d;
+        }
+        // absorption: (M_t - M_s) phi summed, with M_t - M_s = (sigma_t - sigma_s) M
+        for (int e = 0; e < S.nel; ++e) {
+            const double sa = S.sig_t[e] - S.sig_s[e];
+            const double* Te = &S.T[(size_t)e * nb * nb * 4];
+            for (int m = 0; m < nb; ++m)
+                for (int n = 0; n < nb; ++n) absorption += sa * Te[((size_t)m * nb + n) * 4] * phi[(size_t)e * nb + n];
+        }
+        out5[0] = sv;
+        out5[1] = inflow_tot;
+        out5[2] = absorption;
+        out5[3] = outflow;
+        out5[4] = sv + inflow_tot - absorption - outflow;
+        int k = 0;
+        for (const auto& kv : by_attr) {
+            if (k < cap && attrs && vals) {
+                attrs[k] = kv.first;
+                vals[k] = kv.second;
+            }
+            ++k;
+        }
+        if (count) *count = k;
+        return HSW_OK;
+    });
+}
+
+int hsw_device_state(hsw_handle* h, double** psi_a, double** psi_b, double** phi) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_device_state: null handle");
+    if (psi_a) *psi_a = h->d_psiA;
+    if (psi_b) *psi_b = h->d_psiB;
+    if (phi) *phi = h->d_phi;
+    return HSW_OK;
+}
+
+int hsw_sweep_resident(hsw_handle* h) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep_resident: null handle");
+        need_device(h);
+        dev_scatter_source(h->P, h->d_phi, h->d_src, h->stream);
+        run_all_levels(h, h->d_psiA, h->d_psiB, true);
+        h->last_launches += 1;  // scatter-source kernel
+        return HSW_OK;
+    });
+}
+
+int hsw_synchronize(hsw_handle* h) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_synchronize: null handle");
+        need_device(h);
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        check_err(h);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess) h->last_kernel_ms = ms;
+        cudaGetLastError();
+        return HSW_OK;
+    });
+}
+
+void* hsw_stream(hsw_handle* h) { return h ? (void*)h->stream : nullptr; }
+int64_t hsw_last_launch_count(const hsw_handle* h) { return h ? h->last_launches : 0; }
+double hsw_last_sweep_kernel_ms(const hsw_handle* h) { return h ? h->last_kernel_ms : 0.0; }
+
+int hsw_debug_zero_block(hsw_handle* h, int e, int d) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_zero_block: null handle");
+    if (e < 0 || e >= h->S.nel || d < 0 || d >= h->S.nd) return fail(HSW_ERR_RANGE, "hsw_debug_zero_block: out of range");
+    h->zero_pair = (int64_t)e * h->S.nd + d;
+    return HSW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Internal declarations shared by the host setup (hsw_host.cpp), the C ABI
+// (hsw_capi.cpp) and the CUDA kernels (hsw_kernels.cu).  Not installed.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hsw {
+
+// Exception types mapped 1:1 onto hsw_status codes by the C ABI and back onto
+// the reference's exception types by include/hosweep_b200/solver.hpp.
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+constexpr int kMaxFaces = 6;
+constexpr int kMaxFaceNodes = 49;     // (p+1)^2 for p <= 6 (3D p <= 4 -> 25)
+constexpr int kMaxFacePoints = 64;    // (p+2)^2 for p <= 6
+
+// Kernel-facing problem tables (device pointers), POD.
+struct DevProblem {
+    int dim, p, nb, nfn, nqf, nfaces, nel, nd;
+    const double* T;          // [E][nb][nb][4]: M, Gx, Gy, Gz (G_k = -(d_k u)^T W u)
+    const double* sig_t;      // [E]
+    const double* sig_s;      // [E]
+    const double* qvol;       // [E][nb] volume source moments
+    const double* fgeom;      // [E][nfaces][nqf][4]: outward normal (own side), w_q*|J_Gamma|
+    const int* fnbr;          // [E][nfaces][4]: neighbour elem (-1 boundary), neighbour face,
+                              //                 orientation code (own -> neighbour), unused
+    const uint16_t* inflags;  // [nd][E]: bit 2f incoming coupling through face f, bit 2f+1 lagged
+    const double* omega;      // [nd][4]
+    const double* weight;     // [nd]
+    double inflow;
+};
+
+// Host-computed tables that are uploaded to constant memory.
+struct ConstTables {
+    int fnode[kMaxFaces][kMaxFaceNodes];                 // local element node of face node a
+    double trace[kMaxFacePoints][kMaxFaceNodes];         // phi_a(point q) on the reference face
+};
+
+// Device-side launch wrappers (hsw_kernels.cu).
+struct DevState;
+struct LaunchCounters { int64_t launches = 0; };
+
+void dev_upload_tables(const ConstTables& t);
+// scattering + volume source s[e][m] = qvol + (1/4pi) sigma_s M phi
+void dev_scatter_source(const DevProblem& P, const double* phi, double* src, void* stream);
+// one level of the sweep over an explicit pair list
+void dev_sweep_pairs(const DevProblem& P, const double* src, const double* psi_old, double* psi_new,
+                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair,
+                     void* stream);
+// phi = sum_d w_d psi[d] (d ascending), plus max|psi_new - psi_old| and the
+// phi L2 partial sums; deterministic fixed-shape reductions.
+void dev_phi_and_norms(const DevProblem& P, const double* psi_new, const double* psi_old,
+                       const double* phi_old, double* phi_new, double* scratch, double* out3,
+                       void* stream);
+// max_i |a_i - b_i| over n values
+void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scratch, double* out,
+                      void* stream);
+// local solve A_{e,d} x = rhs for a single pair (test hook / API)
+void dev_local_solve(const DevProblem& P, int e, int d, const double* rhs, double* out,
+                     unsigned long long* err_key, int64_t zero_pair, void* stream);
+int dev_max_dynamic_smem_needed(int dim, int p);
+
+}  // namespace hsw
