@@ -1070,7 +1070,7 @@ struct Setup {
                         const double* u = &U[(size_t)q * nb];
                         for (int n = 0; n < nb; ++n) acc[n] += w * u[n];
                     }
-                    for (int n = 0; n < nb; ++n) Te[((size_t)m * nb + n) * 4 + k] = sign * acc[n];
+                    for (int n = 0; n < nb; ++n) Te[((size_t)n * nb + m) * 4 + k] = sign * acc[n];
                 }
             }
             if (!mass_t_cache.empty()) {  // exact reference M_t arithmetic (assembly.hpp:157-158)
@@ -1290,7 +1290,9 @@ struct hsw_handle {
     double *d_omega = nullptr, *d_weight = nullptr;
     double *d_psiA = nullptr, *d_psiB = nullptr, *d_phi = nullptr, *d_phi_old = nullptr, *d_src = nullptr;
     double *d_scratch = nullptr, *d_out = nullptr, *d_vec = nullptr, *d_vec2 = nullptr;
-    int *d_pairs_all = nullptr, *d_pairs_dir = nullptr;
+    int *d_pairs_all = nullptr, *d_pairs_dir = nullptr, *d_pair1 = nullptr;
+    int *d_tab_fnode = nullptr, *d_tab_fidx = nullptr, *d_tab_nmask = nullptr;
+    double *d_tab_trace = nullptr, *d_tab_line = nullptr;
     unsigned long long* d_err = nullptr;
     double* h_out = nullptr;  // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1329,7 +1331,8 @@ void free_handle(hsw_handle* h) {
     if (!h) return;
     void* bufs[] = {h->d_T, h->d_sig_t, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
-                    h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_err};
+                    h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
+                    h->d_err, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->h_out) cudaFreeHost(h->h_out);
@@ -1361,6 +1364,23 @@ void check_err(hsw_handle* h) {
     }
 }
 
+// Kernel selection: the register-resident Gauss-Jordan kernel (hsw_gj.cu) is
+// the product; HSW_KERNEL=v0 selects the simple SMEM reference kernel.
+bool use_v0() {
+    static const bool v0 = [] {
+        const char* k = std::getenv("HSW_KERNEL");
+        return k && std::string(k) == "v0";
+    }();
+    return v0;
+}
+
+void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
+    if (use_v0())
+        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, pairs, n, h->d_err, h->zero_pair, h->stream);
+    else
+        dev_gj_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+}
+
 // All-ordinate sweep psi_old -> psi_new using the current h->d_src.
 void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
     const auto& off = h->S.level_offsets;
@@ -1369,8 +1389,7 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
     for (int l = 0; l < h->S.num_levels; ++l) {
         const int n = off[l + 1] - off[l];
         if (n == 0) continue;
-        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, h->d_pairs_all + off[l], n, h->d_err, h->zero_pair,
-                        h->stream);
+        sweep_launch(h, psi_old, psi_new, h->d_pairs_all + off[l], n);
         ++launches;
     }
     if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
@@ -1383,7 +1402,7 @@ void run_dir_levels(hsw_handle* h, int d, const double* psi_old, double* psi_new
     for (size_t l = 0; l + 1 < off.size(); ++l) {
         const int n = off[l + 1] - off[l];
         if (n == 0) continue;
-        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, base + off[l], n, h->d_err, h->zero_pair, h->stream);
+        sweep_launch(h, psi_old, psi_new, base + off[l], n);
     }
 }
 
@@ -1436,6 +1455,29 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         for (int q = 0; q < S.nqf; ++q)
             for (int a = 0; a < S.nfn; ++a) ct.trace[q][a] = S.trace[(size_t)q * S.nfn + a];
         dev_upload_tables(ct);
+        {
+            std::vector<int> fidx((size_t)kMaxFaces * 128, -1);
+            for (int f = 0; f < S.nf; ++f)
+                for (int a = 0; a < S.nfn; ++a) fidx[(size_t)f * 128 + S.fnodes[f][a]] = a;
+            std::vector<double> line(64, 0.0);
+            for (int i = 0; i < S.face_pts && i < 8; ++i)
+                for (int a = 0; a <= S.p && a < 8; ++a) line[(size_t)i * 8 + a] = S.basis.value(a, S.line_f.x[i]);
+            dev_upload_gj_tables(ct, fidx.data(), line.data());
+            std::vector<int> fn((size_t)kMaxFaces * kMaxFaceNodes, 0), nmask(128, 0);
+            std::vector<double> tr((size_t)kMaxFacePoints * kMaxFaceNodes, 0.0);
+            for (int f = 0; f < kMaxFaces; ++f)
+                for (int a = 0; a < kMaxFaceNodes; ++a) fn[(size_t)f * kMaxFaceNodes + a] = ct.fnode[f][a];
+            for (int q = 0; q < kMaxFacePoints; ++q)
+                for (int a = 0; a < kMaxFaceNodes; ++a) tr[(size_t)q * kMaxFaceNodes + a] = ct.trace[q][a];
+            for (int f = 0; f < kMaxFaces; ++f)
+                for (int m = 0; m < 128; ++m)
+                    if (fidx[(size_t)f * 128 + m] >= 0) nmask[m] |= 1 << f;
+            h->d_tab_fnode = dev_upload(fn);
+            h->d_tab_trace = dev_upload(tr);
+            h->d_tab_fidx = dev_upload(fidx);
+            h->d_tab_nmask = dev_upload(nmask);
+            h->d_tab_line = dev_upload(line);
+        }
         h->d_T = dev_upload(S.T);
         h->d_sig_t = dev_upload(S.sig_t);
         h->d_sig_s = dev_upload(S.sig_s);
@@ -1466,6 +1508,7 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         CUDA_OK(cudaMalloc(&h->d_scratch, (size_t)3 * 65536 * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_out, 8 * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_err, sizeof(unsigned long long)));
+        CUDA_OK(cudaMalloc(&h->d_pair1, sizeof(int)));
         CUDA_OK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
         CUDA_OK(cudaMallocHost(&h->h_out, 8 * sizeof(double)));
         DevProblem& P = h->P;
@@ -1474,6 +1517,8 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         P.T = h->d_T; P.sig_t = h->d_sig_t; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
         P.fgeom = h->d_fgeom; P.fnbr = h->d_fnbr; P.inflags = h->d_inflags;
         P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;
+        P.g_fnode = h->d_tab_fnode; P.g_trace = h->d_tab_trace; P.g_fidx = h->d_tab_fidx;
+        P.g_nmask = h->d_tab_nmask; P.g_line = h->d_tab_line;
         if (desc->check_local_blocks) {
             // SweepSolver ctor factor check (solver.hpp:67-75): one sweep on zero data
             dev_scatter_source(P, h->d_phi, h->d_src, h->stream);
@@ -1564,7 +1609,13 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
             throw hsw::Error(HSW_ERR_RANGE, "hsw_local_solve: element/ordinate out of range");
         const size_t nb = h->S.nb;
         CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        dev_local_solve(h->P, e, d, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        if (use_v0()) {
+            dev_local_solve(h->P, e, d, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        } else {
+            const int pr = e * h->S.nd + d;
+            CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+            dev_gj_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        }
         CUDA_OK(cudaMemcpyAsync(out, h->d_vec2, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         check_err(h);
         return HSW_OK;
@@ -1763,7 +1814,7 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
             const double sa = S.sig_t[e] - S.sig_s[e];
             const double* Te = &S.T[(size_t)e * nb * nb * 4];
             for (int m = 0; m < nb; ++m)
-                for (int n = 0; n < nb; ++n) absorption += sa * Te[((size_t)m * nb + n) * 4] * phi[(size_t)e * nb + n];
+                for (int n = 0; n < nb; ++n) absorption += sa * Te[((size_t)n * nb + m) * 4] * phi[(size_t)e * nb + n];
         }
         out5[0] = sv;
         out5[1] = inflow_tot;
@@ -1818,6 +1869,12 @@ int hsw_synchronize(hsw_handle* h) {
 void* hsw_stream(hsw_handle* h) { return h ? (void*)h->stream : nullptr; }
 int64_t hsw_last_launch_count(const hsw_handle* h) { return h ? h->last_launches : 0; }
 double hsw_last_sweep_kernel_ms(const hsw_handle* h) { return h ? h->last_kernel_ms : 0.0; }
+
+int hsw_debug_flags(hsw_handle* h, int flags) {
+    if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_flags: null handle");
+    h->P.debug_flags = flags;
+    return HSW_OK;
+}
 
 int hsw_debug_zero_block(hsw_handle* h, int e, int d) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_zero_block: null handle");

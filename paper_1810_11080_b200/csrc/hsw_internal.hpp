@@ -23,7 +23,8 @@ constexpr int kMaxFacePoints = 64;    // (p+2)^2 for p <= 6
 // Kernel-facing problem tables (device pointers), POD.
 struct DevProblem {
     int dim, p, nb, nfn, nqf, nfaces, nel, nd;
-    const double* T;          // [E][nb][nb][4]: M, Gx, Gy, Gz (G_k = -(d_k u)^T W u)
+    const double* T;          // [E][n][m][4] (column-major entry (m,n)): M, Gx, Gy, Gz
+                              // with G_k = -(d_k u)^T W u
     const double* sig_t;      // [E]
     const double* sig_s;      // [E]
     const double* qvol;       // [E][nb] volume source moments
@@ -34,6 +35,13 @@ struct DevProblem {
     const double* omega;      // [nd][4]
     const double* weight;     // [nd]
     double inflow;
+    // reference-element tables in global memory (staged into SMEM by the kernels)
+    const int* g_fnode;       // [6][kMaxFaceNodes]
+    const double* g_trace;    // [kMaxFacePoints][kMaxFaceNodes]
+    const int* g_fidx;        // [6][128]
+    const int* g_nmask;       // [128]
+    const double* g_line;     // [8][8]
+    int debug_flags;          // ablation (tools/ablate.py): 1 skip faces, 2 skip elimination, 4 skip T loads
 };
 
 // Host-computed tables that are uploaded to constant memory.
@@ -65,5 +73,12 @@ void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scrat
 void dev_local_solve(const DevProblem& P, int e, int d, const double* rhs, double* out,
                      unsigned long long* err_key, int64_t zero_pair, void* stream);
 int dev_max_dynamic_smem_needed(int dim, int p);
+// production register-resident Gauss-Jordan sweep (hsw_gj.cu)
+void dev_upload_gj_tables(const ConstTables& t, const int* fidx /*6*128*/, const double* line /*8*8*/);
+void dev_gj_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
+                  const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
+void dev_gj_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
+                        unsigned long long* err_key, int64_t zero_pair, void* stream);
+int dev_gj_smem(int dim, int p);
 
 }  // namespace hsw

@@ -92,8 +92,8 @@ __device__ void solve_pair(const DevProblem& pr, int e, int d, const double* __r
     // ---- volume: A = Omega . G + sigma_t M (T[e][m][n] = {M, Gx, Gy, Gz})
     const double4* Te = reinterpret_cast<const double4*>(pr.T) + (size_t)e * NB * NB;
     for (int idx = tid; idx < NB * NB; idx += NT) {
-        const double4 t = Te[idx];
         const int m = idx / NB, n = idx - (idx / NB) * NB;
+        const double4 t = Te[(size_t)n * NB + m];  // column-major T
         double g = om0 * t.y + om1 * t.z;
         if (DIM == 3) g += om2 * t.w;
         A[m * LD + n] = g + st * t.x;
@@ -321,10 +321,10 @@ __global__ void scatter_source_kernel(const DevProblem pr, const double* __restr
     const int nb = pr.nb;
     if (i >= (int64_t)pr.nel * nb) return;
     const int e = (int)(i / nb), m = (int)(i - (i / nb) * nb);
-    const double* Tm = pr.T + ((size_t)e * nb * nb + (size_t)m * nb) * 4;
+    const double* Tm = pr.T + ((size_t)e * nb * nb + (size_t)m) * 4;  // entry (m, n) at (n*nb + m)
     const double* ph = phi + (size_t)e * nb;
     double s = 0.0;
-    for (int n = 0; n < nb; ++n) s += Tm[(size_t)n * 4] * ph[n];
+    for (int n = 0; n < nb; ++n) s += Tm[(size_t)n * nb * 4] * ph[n];
     const double c4pi = 1.0 / (4.0 * 3.14159265358979323846);
     src[i] = pr.qvol[i] + c4pi * (pr.sig_s[e] * s);
 }
