@@ -1874,15 +1874,14 @@ void* orc_create_with_zero_block(const orc_problem* p, int e, int d, char* err, 
         o->diag_override_zero[d].assign(o->nel, 0.0);
         o->diag_override_zero[d][e] = 1.0;
         // re-run the constructor's factorization check with the poked block
-        o->cache_lu = true;
-        o->lu.assign(o->P.quad.size(), {});
+        // (the handle stays in on-the-fly mode, cache_lu = false)
         orc::parallel_for((int)o->P.quad.size(), [&](int dd) {
-            o->lu[dd].resize(o->nel);
             std::vector<double> A((size_t)o->nb * o->nb);
+            orc::DenseLU lu;
             for (int ee = 0; ee < o->nel; ++ee) {
                 o->diag_block(ee, dd, o->ords[dd], A.data());
-                o->lu[dd][ee].factor(A.data(), o->nb);
-                if (!(o->lu[dd][ee].rcond() > 1e-14))
+                lu.factor(A.data(), o->nb);
+                if (!(lu.rcond() > 1e-14))
                     throw orc::SolverError("local streaming+collision block is singular (element " +
                                            std::to_string(ee) + ", ordinate " + std::to_string(dd) + ")");
             }
