@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: element-direction local solves / s per full all-ordinate sweep (FP64).
+
+Contract (see task spec / DESIGN.md §7):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+One "step" = one full sweep of every (element, ordinate) pair of the workload
+(SweepSolver::sweep for all ordinates, solver.hpp:98-117) with the scattering
+source rebuilt from the resident phi.  Inputs (psi, 2 x 4.3 GB at C4) exceed the
+126 MB L2, so no flush is needed between steps.  Rank 0 prints ONE JSON line.
+
+  value      whole-job solves/s, device-resident inputs, CUDA events on the
+             library's stream, max over ranks
+  e2e        same metric through the reference-facing C ABI call hsw_sweep(d=-1)
+             with pinned HOST buffers: H2D psi_old+phi and D2H psi_new inside
+             the timed region
+  roofline   dominant kernel (the Gauss-Jordan sweep kernel): LU-algorithmic
+             FP64 FLOPs F(n) = 2/3 n^3 + 2 n^2 per solve / kernel time, against
+             the FP64 peak measured in-run (DFMA microbenchmark)
+  cpu_baseline  the CPU oracle (port of the reference algorithm) on the host
+             cores, bounded sample of the same workload
+--impl reference times the CPU oracle port alone (the reference itself cannot
+be built here: Eigen/Catch2/CLI11 are absent) on the same config/metric.
+Multi-GPU (N > 1): independent replicas of the full sweep per rank ("weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_TEXT = {
+    "c1": "2D twisted-quad 8x8 Q2, 16 directions (configs[0])",
+    "c2": "2D twisted-quad 128x128 Q3, 64 directions (configs[1])",
+    "c3": "3D twisted-hex 16^3 Q2, 128 directions (configs[2])",
+    "c4": "3D twisted-hex 32^3 Q3, 256 directions (configs[3], production size)",
+    "c5": "3D twisted-hex 24^3 Q4, 256 directions (configs[4], stress case)",
+}
+METRIC = "element-direction local solves/s per full sweep (FP64); % of FP64/HBM roofline"
+UNIT = "solves/s"
+
+
+def flops_per_solve(n: int) -> float:
+    return 2.0 / 3.0 * n ** 3 + 2.0 * n * n
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        under = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(under) if under else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(prob, budget_s: float, threads: int):
+    """Time the CPU oracle (port of the reference algorithm) on a bounded sample."""
+    import numpy as np
+    import oracle as O
+    os.environ["HOSWEEP_THREADS"] = str(threads)
+    nd = prob.num_ordinates
+    ds = list(range(0, nd, max(1, nd // threads)))[:threads]
+    t0 = time.time()
+    orc = O.OracleSolver(prob, cache_lu=False, check_rcond=False, validate=False, active=ds)
+    setup = time.time() - t0
+    phi = np.full(prob.num_dofs, 0.1)
+    # calibrate on a small sample, then run ~budget_s of work
+    t0 = time.time()
+    n0 = orc.sweep_sample(ds, 16, phi)
+    dt0 = max(time.time() - t0, 1e-3)
+    per_solve = dt0 / max(n0, 1)
+    elems = int(max(16, min(prob.num_elements, budget_s / per_solve / len(ds))))
+    t0 = time.time()
+    n = orc.sweep_sample(ds, elems, phi)
+    dt = time.time() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(ds)} ordinates x first {elems} elements of each sweep order "
+                      f"({n} solves, {dt:.1f} s; oracle setup {setup:.1f} s excluded), "
+                      f"on-the-fly local assembly + partial-pivot LU, psi_old = 0",
+            "seconds": dt, "solves": n}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1810_11080_b200 import problem as pb
+    prob = pb.config(args.config)
+    threads = os.cpu_count() or 1
+    steps = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_sample(prob, args.cpu_budget, threads)
+        if i >= args.warmup:
+            steps.append(cb)
+    val = statistics.median(s["value"] for s in steps)
+    pairs = prob.num_elements * prob.num_ordinates
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": pairs / val * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json configs)",
+        "config": {"workload": f"{args.config}: {CONFIG_TEXT[args.config]}", "pairs": pairs,
+                   "n": prob.block_size},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": cb["sample"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference (Eigen-based C++ header library) cannot be built in this image; "
+                "the CPU oracle port of its algorithm is timed (ms_per_step extrapolated to a full sweep)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_1810_11080_b200 as pk
+    from paper_1810_11080_b200 import _capi
+    from paper_1810_11080_b200 import problem as pb
+    import ctypes as C
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    L = _capi.load()
+
+    peak = C.c_double(0.0)
+    rc = L.hsw_fp64_peak(local, C.byref(peak))
+    fp64_peak = peak.value if rc == 0 else None
+
+    prob = pb.config(args.config)
+    t0 = time.time()
+    solver = pk.SweepSolver(prob, device=local)
+    setup_s = time.time() - t0
+    h = solver.handle
+    pairs = prob.num_elements * prob.num_ordinates
+    n = prob.block_size
+    stream = torch.cuda.ExternalStream(L.hsw_stream(h), device=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # resident state: non-trivial phi (scattering source active), psi_old = 0
+    phi0 = np.full(prob.num_dofs, 0.1)
+    assert L.hsw_set_state(h, C.c_void_p(phi0.ctypes.data), None) == 0, _capi.last_error()
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        assert L.hsw_sweep_resident(h) == 0
+        assert L.hsw_synchronize(h) == 0
+    launches_per_step = L.hsw_last_launch_count(h)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rc = L.hsw_sweep_resident(h)
+            assert rc == 0, _capi.last_error()
+            # the per-sweep kernel time (events around the level launches) is read
+            # after the region; synchronising here would not change device time
+            ev_mid = None
+        ev1.record(stream)
+    torch.cuda.synchronize()
+    rc = L.hsw_synchronize(h)
+    assert rc == 0, _capi.last_error()
+    barrier()
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    # kernel-only time of one sweep (events around the sweep-kernel launches)
+    for _ in range(2):
+        L.hsw_sweep_resident(h)
+        L.hsw_synchronize(h)
+        kernel_ms.append(L.hsw_last_sweep_kernel_ms(h))
+    kms = min(kernel_ms)
+    ms_step = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * pairs / (ms_step * 1e-3)
+
+    # ---- end-to-end through the reference-facing ABI call with pinned host buffers
+    e2e = None
+    if not args.skip_e2e:
+        N = prob.num_dofs
+        nd = prob.num_ordinates
+        phi_h = torch.full((N,), 0.1, dtype=torch.float64).pin_memory()
+        psi_old_h = torch.zeros((nd, N), dtype=torch.float64).pin_memory()
+        psi_new_h = torch.empty((nd, N), dtype=torch.float64).pin_memory()
+        vp = C.c_void_p
+        for _ in range(1):
+            assert L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr())) == 0
+        e2e_steps = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            rc = L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr()))
+            assert rc == 0, _capi.last_error()
+            psi_old_h, psi_new_h = psi_new_h, psi_old_h
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * pairs / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": (nd * N + N) * 8, "d2h_bytes_per_step": nd * N * 8,
+               "ms_per_step": e2e_s * 1e3, "api": "hsw_sweep(h, -1, phi, psi_old, psi_new) host pointers"}
+        del phi_h, psi_old_h, psi_new_h
+
+    # ---- roofline of the dominant kernel (the sweep kernel)
+    achieved = flops_per_solve(n) * pairs / (kms * 1e-3) * 1e-12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": (achieved / fp64_peak) if fp64_peak else None, "traffic": traffic,
+                "peak_source": "measured in-run: DFMA-chain microbenchmark over all SMs "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "flops_per_solve": flops_per_solve(n), "kernel_ms_per_sweep": kms,
+                "kernel_launches_per_sweep": launches_per_step - 1}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        try:
+            cpu = cpu_sample(prob, args.cpu_budget, os.cpu_count() or 1)
+            cpu.pop("seconds", None)
+            cpu.pop("solves", None)
+        except Exception as ex:  # the baseline is reported, never the product
+            cpu = {"value": None, "unit": UNIT, "error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json configs, seeded)",
+            "config": {"workload": f"{args.config}: {CONFIG_TEXT[args.config]}", "pairs": pairs, "n": n,
+                       "levels": solver.num_levels, "l2": "inputs larger than L2 (psi 2 x "
+                       f"{prob.num_ordinates * prob.num_dofs * 8 / 1e9:.2f} GB)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "setup_s": round(setup_s, 2)},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": int(launches_per_step * args.steps),
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIG_TEXT))
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -182,6 +182,9 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
 /* ---- device-resident state for benchmarking / advanced callers ---------- */
 /* Device pointers of the handle's psi (two buffers, [nd][N] each) and phi. */
 int hsw_device_state(hsw_handle* h, double** psi_a, double** psi_b, double** phi);
+/* Copy host phi (N) and/or psi (nd*N, into psi_a) into the resident device
+ * state; either pointer may be NULL. */
+int hsw_set_state(hsw_handle* h, const double* phi, const double* psi);
 /* One all-ordinate sweep psi_a -> psi_b with the current device phi (the
  * scattering source is rebuilt inside), stream-ordered; no host sync. */
 int hsw_sweep_resident(hsw_handle* h);
@@ -194,6 +197,15 @@ int64_t hsw_last_launch_count(const hsw_handle* h);
 /* Device time of the main sweep kernel launches of the last
  * hsw_sweep_resident call, measured with CUDA events on the handle's stream. */
 double hsw_last_sweep_kernel_ms(const hsw_handle* h);
+
+/* Measured FP64 FMA throughput of the device (TFLOP/s) from a DFMA-chain
+ * microbenchmark over all SMs (~0.1 s); the roofline denominator of the
+ * sweep kernel.  device: CUDA ordinal. */
+int hsw_fp64_peak(int device, double* tflops);
+
+/* Ablation switches for development timing (results are NOT valid solves):
+ * 1 skip the face terms, 2 skip the elimination, 4 skip the tensor loads. */
+int hsw_debug_flags(hsw_handle* h, int flags);
 
 /* Test hook mirroring test_solver.cpp:332-344 (op.ordinates[d].diag[e].setZero()):
  * zero the assembled local block of (e, d) in every later factorization. */

@@ -70,6 +70,8 @@ def lib():
         L.orc_sweep_all.argtypes = [vp, vp, vp, vp, cp, C.c_int]
         L.orc_sweep_subset.argtypes = [vp, C.c_int, vp, vp, vp, cp, C.c_int]
         L.orc_direct_oracle.argtypes = [vp, C.c_int, vp, vp, cp, C.c_int]
+        L.orc_sweep_sample.argtypes = [vp, C.c_int, vp, C.c_int, vp, cp, C.c_int]
+        L.orc_sweep_sample.restype = C.c_longlong
         L.orc_source_iteration.argtypes = [vp, C.c_double, C.c_int, C.c_int, vp, vp, vp, vp, vp, cp, C.c_int]
         L.orc_balance.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int]
         L.orc_graph_tarjan.argtypes = [C.c_int, C.c_int, vp, vp]
@@ -235,6 +237,17 @@ class OracleSolver:
         err = C.create_string_buffer(1024)
         self._check(lib().orc_sweep_subset(self.h, len(ds), _p(ds), _p(phi), _p(out), err, 1024), err)
         return out
+
+    def sweep_sample(self, ds, max_elems: int, phi) -> int:
+        """Bounded CPU-baseline sample: the first max_elems elements of each
+        listed ordinate's sweep (on-the-fly local assembly + LU); returns solves."""
+        ds = np.ascontiguousarray(ds, np.int32)
+        phi = np.ascontiguousarray(phi, np.float64)
+        err = C.create_string_buffer(1024)
+        n = lib().orc_sweep_sample(self.h, len(ds), _p(ds), max_elems, _p(phi), err, 1024)
+        if n < 0:
+            raise OracleError(err.value.decode())
+        return int(n)
 
     def direct_oracle(self, d: int, phi) -> np.ndarray:
         phi = np.ascontiguousarray(phi, np.float64)

@@ -1770,6 +1770,55 @@ int orc_sweep_subset(void* h, int nd, const int* ds, const double* phi, double* 
         return 0;
     } catch (const std::exception& ex) { set_err(ex.what(), err, errlen); return 1; }
 }
+// Bounded CPU-baseline sample: for each listed ordinate, the first max_elems
+// elements of its sweep order (the reference's per-element work: assemble the
+// local block on the fly, factor, solve), psi_old = 0, one ordinate per thread.
+// Returns the number of (element, ordinate) solves performed.
+long long orc_sweep_sample(void* h, int nd, const int* ds, int max_elems, const double* phi, char* err,
+                           int errlen) {
+    try {
+        auto* o = static_cast<orc::Oracle*>(h);
+        const size_t N = (size_t)o->nel * o->nb;
+        std::atomic<long long> count{0};
+        orc::parallel_for(nd, [&](int i) {
+            const int d = ds[i];
+            const orc::PerOrdinate& ord = o->ords[d];
+            std::vector<double> psi(N, 0.0), zero(N, 0.0), rhs(o->nb), A((size_t)o->nb * o->nb);
+            orc::DenseLU lu;
+            const int nfn = o->nf_nodes;
+            const double c4pi = 1.0 / (4.0 * M_PI);
+            const int ne = std::min<int>(max_elems, (int)ord.order.size());
+            for (int q = 0; q < ne; ++q) {
+                const int e = ord.order[q];
+                for (int m = 0; m < o->nb; ++m)
+                    rhs[m] = o->src_vol[(size_t)e * o->nb + m] + ord.src_bnd[(size_t)e * o->nb + m];
+                const auto& ms = o->mass_scatter[e];
+                for (int m = 0; m < o->nb; ++m) {
+                    double s = 0.0;
+                    for (int n = 0; n < o->nb; ++n) s += ms[(size_t)m * o->nb + n] * phi[(size_t)e * o->nb + n];
+                    rhs[m] += c4pi * s;
+                }
+                for (int c : ord.incoming[e]) {
+                    const orc::Coupling& fc = ord.couplings[c];
+                    const double* src = ord.lagged[c] ? zero.data() : psi.data();
+                    const auto& dn = o->fnodes[fc.down_face];
+                    const auto& un = o->fnodes[fc.up_face];
+                    for (int m = 0; m < nfn; ++m) {
+                        double s = 0.0;
+                        for (int n = 0; n < nfn; ++n) s += fc.block[m * nfn + n] * src[(size_t)fc.upwind * o->nb + un[n]];
+                        rhs[dn[m]] -= s;
+                    }
+                }
+                o->diag_block(e, d, ord, A.data());
+                lu.factor(A.data(), o->nb);
+                lu.solve(rhs.data(), &psi[(size_t)e * o->nb]);
+            }
+            count += ne;
+        });
+        return count.load();
+    } catch (const std::exception& ex) { set_err(ex.what(), err, errlen); return -1; }
+}
+
 int orc_direct_oracle(void* h, int d, const double* phi, double* psi, char* err, int errlen) {
     try {
         static_cast<orc::Oracle*>(h)->direct_oracle(d, phi, psi);

@@ -27,6 +27,7 @@ EXPORTED = [
     "hsw_sweep", "hsw_sweep_device", "hsw_direct_oracle", "hsw_source_iteration", "hsw_balance",
     "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
     "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
+    "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state",
 ]
 
 
@@ -92,6 +93,9 @@ def load():
     L.hsw_last_sweep_kernel_ms.argtypes = [vp]
     L.hsw_last_sweep_kernel_ms.restype = C.c_double
     L.hsw_debug_zero_block.argtypes = [vp, C.c_int, C.c_int]
+    L.hsw_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    L.hsw_debug_flags.argtypes = [vp, C.c_int]
+    L.hsw_set_state.argtypes = [vp, vp, vp]
     _lib = L
     return L
 

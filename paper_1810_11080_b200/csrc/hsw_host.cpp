@@ -1842,6 +1842,19 @@ int hsw_device_state(hsw_handle* h, double** psi_a, double** psi_b, double** phi
     return HSW_OK;
 }
 
+int hsw_set_state(hsw_handle* h, const double* phi, const double* psi) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_set_state: null handle");
+        need_device(h);
+        if (phi) CUDA_OK(cudaMemcpyAsync(h->d_phi, phi, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        if (psi)
+            CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi, h->N * h->S.nd * sizeof(double), cudaMemcpyHostToDevice,
+                                    h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        return HSW_OK;
+    });
+}
+
 int hsw_sweep_resident(hsw_handle* h) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep_resident: null handle");
@@ -1869,6 +1882,17 @@ int hsw_synchronize(hsw_handle* h) {
 void* hsw_stream(hsw_handle* h) { return h ? (void*)h->stream : nullptr; }
 int64_t hsw_last_launch_count(const hsw_handle* h) { return h ? h->last_launches : 0; }
 double hsw_last_sweep_kernel_ms(const hsw_handle* h) { return h ? h->last_kernel_ms : 0.0; }
+
+int hsw_fp64_peak(int device, double* tflops) {
+    return guarded([&] {
+        if (!tflops) throw hsw::Error(HSW_ERR_INVALID, "hsw_fp64_peak: null output");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw hsw::Error(HSW_ERR_CUDA, "hsw_fp64_peak: no CUDA device");
+        *tflops = dev_fp64_peak_tflops(device);
+        return HSW_OK;
+    });
+}
 
 int hsw_debug_flags(hsw_handle* h, int flags) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_flags: null handle");

@@ -73,6 +73,7 @@ void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scrat
 void dev_local_solve(const DevProblem& P, int e, int d, const double* rhs, double* out,
                      unsigned long long* err_key, int64_t zero_pair, void* stream);
 int dev_max_dynamic_smem_needed(int dim, int p);
+double dev_fp64_peak_tflops(int device);
 // production register-resident Gauss-Jordan sweep (hsw_gj.cu)
 void dev_upload_gj_tables(const ConstTables& t, const int* fidx /*6*128*/, const double* line /*8*8*/);
 void dev_gj_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,

@@ -425,6 +425,53 @@ maxdiff_kernel(const double* __restrict__ a, const double* __restrict__ b, int64
     }
 }
 
+// ------------------------------------------------ FP64 peak microbenchmark
+// 8 independent DFMA chains per thread, all SMs busy: the measured FP64
+// roofline denominator (the sweep's FLOPs are FP64 FMAs on the CUDA cores).
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double s) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            a0 = fma(a0, m, s); a1 = fma(a1, m, s); a2 = fma(a2, m, s); a3 = fma(a3, m, s);
+            a4 = fma(a4, m, s); a5 = fma(a5, m, s); a6 = fma(a6, m, s); a7 = fma(a7, m, s);
+        }
+    }
+    const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 12345.678) out[0] = r;  // keep the chains alive
+}
+
+double dev_fp64_peak_tflops(int device) {
+    KCHECK(cudaSetDevice(device));
+    int sms = 0;
+    KCHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* out = nullptr;
+    KCHECK(cudaMalloc(&out, sizeof(double)));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    fp64_peak_kernel<<<blocks, threads>>>(out, 16, 1e-3);  // warm-up
+    KCHECK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    KCHECK(cudaEventCreate(&e0));
+    KCHECK(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        KCHECK(cudaEventRecord(e0));
+        fp64_peak_kernel<<<blocks, threads>>>(out, iters, 1e-3);
+        KCHECK(cudaEventRecord(e1));
+        KCHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        KCHECK(cudaEventElapsedTime(&ms, e0, e1));
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 8.0 * 16.0 * (double)iters * (double)blocks * threads;
+    return flops / (best * 1e-3) * 1e-12;
+}
+
 void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scratch, double* out, void* stream) {
     const int nblk = (int)std::min<int64_t>(kRedBlocks, (n + kRedThreads - 1) / kRedThreads);
     cudaStream_t st = (cudaStream_t)stream;

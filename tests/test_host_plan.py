@@ -71,7 +71,7 @@ def test_full_c1_and_c2_cut_sets():
 
 def test_abi_exports_every_declared_symbol():
     hdr = open(os.path.join(ROOT, "include", "hosweep_b200.h")).read()
-    declared = set(re.findall(r"\b(hsw_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(hsw_[a-z0-9_]+)\s*\(", hdr))
     assert declared == set(_capi.EXPORTED), declared ^ set(_capi.EXPORTED)
     lib = C.CDLL(_capi.LIB_PATH)
     for sym in declared:
