@@ -206,6 +206,9 @@ int hsw_fp64_peak(int device, double* tflops);
 /* Ablation switches for development timing (results are NOT valid solves):
  * 1 skip the face terms, 2 skip the elimination, 4 skip the tensor loads. */
 int hsw_debug_flags(hsw_handle* h, int flags);
+/* Debug phase-cycle counters of flag 8 (table staging, faces, assembly,
+ * elimination, write-back, pair count; 8-11: panel wait, U, DMMA, factor). */
+int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]);
 
 /* Test hook mirroring test_solver.cpp:332-344 (op.ordinates[d].diag[e].setZero()):
  * zero the assembled local block of (e, d) in every later factorization. */

@@ -27,7 +27,7 @@ EXPORTED = [
     "hsw_sweep", "hsw_sweep_device", "hsw_direct_oracle", "hsw_source_iteration", "hsw_balance",
     "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
     "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
-    "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state",
+    "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
 ]
 
 
@@ -96,6 +96,7 @@ def load():
     L.hsw_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.hsw_debug_flags.argtypes = [vp, C.c_int]
     L.hsw_set_state.argtypes = [vp, vp, vp]
+    L.hsw_debug_profile.argtypes = [vp, vp]
     _lib = L
     return L
 

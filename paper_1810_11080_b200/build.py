@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["hsw_kernels.cu", "hsw_gj.cu"]
+SOURCES_CU = ["hsw_kernels.cu", "hsw_gj.cu", "hsw_dmma.cu"]
 SOURCES_CPP = ["hsw_host.cpp"]
 HEADERS = ["hsw_internal.hpp", os.path.join(ROOT, "include", "hosweep_b200.h")]
 
@@ -50,7 +50,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(objdir, s + ".o")
         if force or _stale(obj, [src] + hdrs):
-            cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
+            dbg = ["-DHSW_DEBUG_BOUNDS"] if os.environ.get("HSW_DEBUG_BOUNDS") == "1" else []
+            cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", *dbg,
                    "--expt-relaxed-constexpr", *inc, "-c", src, "-o", obj]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")

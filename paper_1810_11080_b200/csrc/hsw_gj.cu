@@ -65,8 +65,9 @@ struct GJ {
     static constexpr int L = 32 / PPW;                       // lanes per pair
     static constexpr int R = (N + L - 1) / L;                // rows per lane
     static constexpr int SB = 4;                             // column slots per skip block
-    static constexpr int CW = ((NC + W - 1) / W + SB - 1) / SB * SB;  // slots per warp (whole blocks)
-    static constexpr int NBLK = CW / SB;
+    // block-cyclic columns: blocks of SB consecutive columns, block b -> warp b % W
+    static constexpr int NBLK = ((NC + SB - 1) / SB + W - 1) / W;  // blocks per warp
+    static constexpr int CW = NBLK * SB;                     // slots per warp
     static constexpr int NFN = DIM == 2 ? N1 : N1 * N1;
     static constexpr int NF = 2 * DIM;
     static constexpr int NQ1 = P + 2;                        // face Gauss points per axis
@@ -114,6 +115,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
     constexpr int NQ1 = G::NQ1, NQF = G::NQF, N1 = G::N1, SB = G::SB, NBLK = G::NBLK, T1SZ = G::T1SZ;
     extern __shared__ double smem[];
 
+    const long long t_start = clock64();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int group = warp / W, w = warp - group * W;       // pair group, warp within group
     const int ps = lane / L, ll = lane - ps * L;             // pair slot within warp, lane within pair
@@ -133,6 +135,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
     for (int idx = threadIdx.x; idx < NQ1 * N1; idx += G::THREADS)
         s_line[idx] = __ldg(pr.g_line + (idx / N1) * 8 + idx % N1);
     __syncthreads();
+    const long long t_tab = clock64();
     double* gsm = smem + G::TAB_TOTAL + (size_t)group * G::SM_GROUP;
     double* psm = gsm + ps * G::SM_PAIR;                      // this pair's scratch
     double* lbuf = gsm + PPW * G::SM_PAIR;                    // W > 1 multipliers (double-buffered)
@@ -163,6 +166,33 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
 
     // ------------------------------------------------ faces, phase 1: weights + upwind gathers
     const int dbg = pr.debug_flags;
+    // ------------------------------------------------ volume terms straight into registers
+    // (issued before the face phase so the T-tensor loads overlap it; branch-free
+    // so the compiler can batch the loads)
+    double a[R][CW];
+    {
+        const double st = pr.sig_t[e];
+        const double4* Te = reinterpret_cast<const double4*>(pr.T) + (size_t)e * N * N;
+#pragma unroll
+        for (int s = 0; s < CW; ++s) {
+            const int j = ((s / SB) * W + w) * SB + (s % SB);
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int r = ll + L * i;
+                double v = 0.0;
+                if (r < N && j < N) {
+                    const double4 t = (dbg & 4) ? make_double4(r == j ? 1.0 : 0.0, 0.0, 0.0, 0.0)
+                                                : Te[(size_t)j * N + r];  // column-major: coalesced over rows
+                    double g = om0 * t.y + om1 * t.z;
+                    if (DIM == 3) g += om2 * t.w;
+                    v = g + st * t.x;
+                } else if (r < N && j == N) {
+                    v = rhs_given ? rhs_given[r] : src[(size_t)e * N + r];
+                }
+                a[i][s] = v;
+            }
+        }
+    }
     if (ctid == 0) { flg[0] = 0; flg[1] = 0; }
     pair_sync();
     int outm = 0, inm = 0;
@@ -249,11 +279,11 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
     pair_sync();
     }  // dbg & 1
 
+    const long long t_face = clock64();
     // ------------------------------------------------ assemble into registers
-    double a[R][CW];
     {
-        const double st = pr.sig_t[e];
-        const double4* Te = reinterpret_cast<const double4*>(pr.T) + (size_t)e * N * N;
+        // face contributions: outflow blocks on (face-node row, face-node column)
+        // entries and inflow projections on the rhs column
         int rmask[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -262,26 +292,19 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
         }
 #pragma unroll
         for (int s = 0; s < CW; ++s) {
-            const int j = s * W + w;
+            const int j = ((s / SB) * W + w) * SB + (s % SB);
             const int cmask = j < N ? s_nmask[j] : 0;
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 const int r = ll + L * i;
-                double v = 0.0;
                 if (r < N && j < N) {
-                    const double4 t = (dbg & 4) ? make_double4(r == j ? 1.0 : 0.0, 0.0, 0.0, 0.0)
-                                                : Te[(size_t)j * N + r];  // column-major: coalesced over rows
-                    double g = om0 * t.y + om1 * t.z;
-                    if (DIM == 3) g += om2 * t.w;
-                    v = g + st * t.x;
                     int m = rmask[i] & cmask;
                     while (m) {  // outflow blocks of the faces shared by node r and node j
                         const int f = __ffs(m) - 1;
                         m &= m - 1;
-                        v += FM[f * NFN * NFN + s_fidx[f * N + r] * NFN + s_fidx[f * N + j]];
+                        a[i][s] += FM[f * NFN * NFN + s_fidx[f * N + r] * NFN + s_fidx[f * N + j]];
                     }
                 } else if (r < N && j == N) {
-                    v = rhs_given ? rhs_given[r] : src[(size_t)e * N + r];
                     int m = s_nmask[r] & (inm | (inm >> 8)) & 63;
                     while (m) {
                         const int f = __ffs(m) - 1;
@@ -289,10 +312,9 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
                         const int fr = s_fidx[f * N + r];
                         double s2 = 0.0;
                         for (int q = 0; q < NQF; ++q) s2 += TR[f * NQF + q] * s_trace[q * NFN + fr];
-                        v += s2;
+                        a[i][s] += s2;
                     }
                 }
-                a[i][s] = v;
             }
         }
     }
@@ -301,7 +323,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
         for (int i = 0; i < R; ++i)
 #pragma unroll
             for (int s = 0; s < CW; ++s)
-                if (s * W + w < N) a[i][s] = 0.0;
+                if (((s / SB) * W + w) * SB + (s % SB) < N) a[i][s] = 0.0;
     }
     // matrix scale for the singularity test (stand-in for rcond > 1e-14, solver.hpp:70)
     double amax = 0.0;
@@ -309,7 +331,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
     for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int s = 0; s < CW; ++s)
-            if (s * W + w < N) amax = fmax(amax, fabs(a[i][s]));
+            if (((s / SB) * W + w) * SB + (s % SB) < N) amax = fmax(amax, fabs(a[i][s]));
 #pragma unroll
     for (int off = L / 2; off > 0; off >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
     if (W > 1) {
@@ -319,6 +341,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
         for (int q = 0; q < W; ++q) amax = fmax(amax, amx[q]);
     }
 
+    const long long t_asm = clock64();
     // ------------------------------------------------ Gauss-Jordan
     // Lookahead 1: inside step k the owner warp of column k+1 updates that
     // column first, searches pivot k+1 and publishes its multipliers before its
@@ -385,7 +408,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
         }
     };
     auto consume = [&](int k, double (&lo)[R], int& prow_o, double& piv_o) {
-        while (*ready < k) {}
+        while (*ready < k) __nanosleep(32);
         __threadfence_block();
         const double* slot = ring + (k & 7) * RS;
 #pragma unroll
@@ -421,85 +444,85 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
     if (W > 1 && w != 0) consume(0, l, prow, piv);
     mark(0, prow, piv);
 
+    // step k = ((sb * W + o) * SB + t): block sb of owner warp o, slot sb*SB + t
 #pragma unroll
-    for (int s = 0; s < CW; ++s) {
+    for (int sb = 0; sb < NBLK; ++sb) {
 #pragma unroll 1
         for (int o = 0; o < W; ++o) {
-            const int k = s * W + o;
-            if (k >= N) break;
-            // publish the pivot row's segment of this warp's slots >= s
-            const int pslot = prow / L, plane = prow % L;
 #pragma unroll
-            for (int i = 0; i < R; ++i) {
-                if (i == pslot && ll == plane) {
+            for (int t = 0; t < SB; ++t) {
+                const int s = sb * SB + t;
+                const int k = (sb * W + o) * SB + t;
+                if (k < N) {
+                    // publish the pivot row's segment of this warp's blocks >= sb
+                    const int pslot = prow / L, plane = prow % L;
 #pragma unroll
-                    for (int s2 = s & ~1; s2 < CW; s2 += 2)
-                        *reinterpret_cast<double2*>(ubuf + s2) = make_double2(a[i][s2], a[i][s2 + 1]);
-                }
-            }
-            __syncwarp();
-            // slots s, s+1 first (they hold column k+1 for its owner warp)
-            {
-                const double2 u2 = *reinterpret_cast<const double2*>(ubuf + (s & ~1));
-                if (s & 1) {
+                    for (int i = 0; i < R; ++i) {
+                        if (i == pslot && ll == plane) {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) a[i][s] -= l[i] * u2.y;
-                } else {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) a[i][s] -= l[i] * u2.x;
-                    if (s + 1 < CW) {
-#pragma unroll
-                        for (int i = 0; i < R; ++i) a[i][s + 1 < CW ? s + 1 : 0] -= l[i] * u2.y;
+                            for (int s2 = sb * SB; s2 < CW; s2 += 2)
+                                *reinterpret_cast<double2*>(ubuf + s2) = make_double2(a[i][s2], a[i][s2 + 1]);
+                        }
                     }
+                    __syncwarp();
+                    // block sb (+ the first pair of block sb+1) first: they hold column k+1
+                    const int FIRST_END = (sb + 1) * SB + 2 < CW ? (sb + 1) * SB + 2 : CW;
+#pragma unroll
+                    for (int s2 = sb * SB; s2 < FIRST_END; s2 += 2) {
+                        const double2 u2 = *reinterpret_cast<const double2*>(ubuf + s2);
+#pragma unroll
+                        for (int i = 0; i < R; ++i) {
+                            a[i][s2] -= l[i] * u2.x;
+                            a[i][s2 + 1] -= l[i] * u2.y;
+                        }
+                    }
+                    const int kn = k + 1;
+                    const int own_n = W == 1 ? 0 : (t < SB - 1 ? o : (o + 1 == W ? 0 : o + 1));
+                    double ln[R];
+                    int prown = 0;
+                    double pivn = 1.0;
+                    if (kn < N && w == own_n) {
+                        double cv[R];
+#pragma unroll
+                        for (int i = 0; i < R; ++i) {
+                            if (t < SB - 1) cv[i] = a[i][s + 1 < CW ? s + 1 : 0];
+                            else if (W > 1 && o + 1 < W) cv[i] = a[i][sb * SB];
+                            else cv[i] = a[i][(sb + 1) * SB < CW ? (sb + 1) * SB : 0];
+                        }
+                        search(cv, ln, prown, pivn);
+                        if (W > 1) produce(kn, ln, prown, pivn);
+                    }
+                    // bulk update of the remaining slots with step k
+#pragma unroll
+                    for (int s2 = FIRST_END; s2 < CW; s2 += 2) {
+                        const double2 u2 = *reinterpret_cast<const double2*>(ubuf + s2);
+#pragma unroll
+                        for (int i = 0; i < R; ++i) {
+                            a[i][s2] -= l[i] * u2.x;
+                            a[i][s2 + 1] -= l[i] * u2.y;
+                        }
+                    }
+                    __syncwarp();  // ubuf reads complete before the next publication
+                    if (kn < N) {
+                        if (W > 1 && w != own_n) consume(kn, ln, prown, pivn);
+#pragma unroll
+                        for (int i = 0; i < R; ++i) l[i] = ln[i];
+                        prow = prown;
+                        piv = pivn;
+                        mark(kn, prow, piv);
+                    }
+                    if (W > 1 && t == SB - 1) pair_sync();  // bounds the 8-slot multiplier ring
                 }
-                if ((s & 1) && s + 1 < CW) {
-                    const double u1 = ubuf[s + 1 < CW ? s + 1 : 0];
-#pragma unroll
-                    for (int i = 0; i < R; ++i) a[i][s + 1 < CW ? s + 1 : 0] -= l[i] * u1;
-                }
             }
-            const int kn = k + 1;
-            const int own_n = W == 1 ? 0 : (o + 1 == W ? 0 : o + 1);
-            double ln[R];
-            int prown = 0;
-            double pivn = 1.0;
-            if (kn < N && w == own_n) {
-                double cv[R];
-#pragma unroll
-                for (int i = 0; i < R; ++i)
-                    cv[i] = (W > 1 && o + 1 < W) ? a[i][s] : a[i][s + 1 < CW ? s + 1 : s];
-                search(cv, ln, prown, pivn);
-                if (W > 1) produce(kn, ln, prown, pivn);
-            }
-            // bulk update of slots >= s+2 with step k
-#pragma unroll
-            for (int s2 = (s + 2) & ~1; s2 < CW; s2 += 2) {
-                const double2 u2 = *reinterpret_cast<const double2*>(ubuf + s2);
-                if (s2 >= s + 2) {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) a[i][s2] -= l[i] * u2.x;
-                }
-#pragma unroll
-                for (int i = 0; i < R; ++i) a[i][s2 + 1] -= l[i] * u2.y;
-            }
-            __syncwarp();  // ubuf reads complete before the next publication
-            if (kn < N) {
-                if (W > 1 && w != own_n) consume(kn, ln, prown, pivn);
-#pragma unroll
-                for (int i = 0; i < R; ++i) l[i] = ln[i];
-                prow = prown;
-                piv = pivn;
-                mark(kn, prow, piv);
-            }
-            if (W > 1 && (k & 3) == 3) pair_sync();
         }
     }
     if (W > 1) pair_sync();
     else __syncwarp();
 
+    const long long t_gj = clock64();
     // ------------------------------------------------ solution x_k = rhs(p_k) / pivot_k
     if (singular && active && ll == 0) atomicMin(err_key, (unsigned long long)pair);
-    constexpr int SN = N % W, SSLOT = N / W;  // warp / slot holding the rhs column
+    constexpr int SN = (N / SB) % W, SSLOT = ((N / SB) / W) * SB + N % SB;  // warp / slot of the rhs column
     if (active && w == SN) {
         double* out = rhs_given ? psi_out : psi_out + (size_t)d * psi_stride + (size_t)e * N;
 #pragma unroll
@@ -510,6 +533,15 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
                 out[kk] = a[i][SSLOT] / pivval[kk];
             }
         }
+    }
+    if ((dbg & 8) && lane == 0 && w == 0 && ps == 0 && active) {
+        const long long t_end = clock64();
+        atomicAdd(pr.prof + 0, (unsigned long long)(t_tab - t_start));
+        atomicAdd(pr.prof + 1, (unsigned long long)(t_face - t_tab));
+        atomicAdd(pr.prof + 2, (unsigned long long)(t_asm - t_face));
+        atomicAdd(pr.prof + 3, (unsigned long long)(t_gj - t_asm));
+        atomicAdd(pr.prof + 4, (unsigned long long)(t_end - t_gj));
+        atomicAdd(pr.prof + 5, 1ull);
     }
 }
 

@@ -1291,6 +1291,7 @@ struct hsw_handle {
     double *d_psiA = nullptr, *d_psiB = nullptr, *d_phi = nullptr, *d_phi_old = nullptr, *d_src = nullptr;
     double *d_scratch = nullptr, *d_out = nullptr, *d_vec = nullptr, *d_vec2 = nullptr;
     int *d_pairs_all = nullptr, *d_pairs_dir = nullptr, *d_pair1 = nullptr;
+    unsigned long long* d_prof = nullptr;
     int *d_tab_fnode = nullptr, *d_tab_fidx = nullptr, *d_tab_nmask = nullptr;
     double *d_tab_trace = nullptr, *d_tab_line = nullptr;
     unsigned long long* d_err = nullptr;
@@ -1332,7 +1333,7 @@ void free_handle(hsw_handle* h) {
     void* bufs[] = {h->d_T, h->d_sig_t, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
                     h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
-                    h->d_err, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
+                    h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->h_out) cudaFreeHost(h->h_out);
@@ -1366,19 +1367,35 @@ void check_err(hsw_handle* h) {
 
 // Kernel selection: the register-resident Gauss-Jordan kernel (hsw_gj.cu) is
 // the product; HSW_KERNEL=v0 selects the simple SMEM reference kernel.
-bool use_v0() {
-    static const bool v0 = [] {
+// Kernel selection: "dmma" (default, hsw_dmma.cu), "gj" (register-resident
+// DFMA Gauss-Jordan, hsw_gj.cu) or "v0" (simple SMEM LU, hsw_kernels.cu).
+// HSW_KERNEL=auto (default) picks the faster measured kernel per shape
+// (profiles/: DMMA for 2D, register Gauss-Jordan for 3D p >= 2).
+int kernel_choice_env() {
+    static const int kc = [] {
         const char* k = std::getenv("HSW_KERNEL");
-        return k && std::string(k) == "v0";
+        if (k && std::string(k) == "v0") return 0;
+        if (k && std::string(k) == "gj") return 1;
+        if (k && std::string(k) == "dmma") return 2;
+        return -1;
     }();
-    return v0;
+    return kc;
 }
+int kernel_choice_for(int dim, int p) {
+    const int env = kernel_choice_env();
+    if (env >= 0) return env;
+    return (dim == 3 && p >= 2) ? 1 : 2;
+}
+thread_local int g_kernel_dim = 2, g_kernel_p = 1;
+int kernel_choice() { return kernel_choice_for(g_kernel_dim, g_kernel_p); }
+bool use_v0() { return kernel_choice() == 0; }
 
 void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
-    if (use_v0())
-        dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, pairs, n, h->d_err, h->zero_pair, h->stream);
-    else
-        dev_gj_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+    switch (kernel_choice_for(h->S.dim, h->S.p)) {
+        case 0: dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, pairs, n, h->d_err, h->zero_pair, h->stream); break;
+        case 1: dev_gj_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream); break;
+        default: dev_dmma_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+    }
 }
 
 // All-ordinate sweep psi_old -> psi_new using the current h->d_src.
@@ -1509,6 +1526,8 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         CUDA_OK(cudaMalloc(&h->d_out, 8 * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_err, sizeof(unsigned long long)));
         CUDA_OK(cudaMalloc(&h->d_pair1, sizeof(int)));
+        CUDA_OK(cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
         CUDA_OK(cudaMallocHost(&h->h_out, 8 * sizeof(double)));
         DevProblem& P = h->P;
@@ -1519,6 +1538,7 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;
         P.g_fnode = h->d_tab_fnode; P.g_trace = h->d_tab_trace; P.g_fidx = h->d_tab_fidx;
         P.g_nmask = h->d_tab_nmask; P.g_line = h->d_tab_line;
+        P.prof = h->d_prof;
         if (desc->check_local_blocks) {
             // SweepSolver ctor factor check (solver.hpp:67-75): one sweep on zero data
             dev_scatter_source(P, h->d_phi, h->d_src, h->stream);
@@ -1609,12 +1629,17 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
             throw hsw::Error(HSW_ERR_RANGE, "hsw_local_solve: element/ordinate out of range");
         const size_t nb = h->S.nb;
         CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        g_kernel_dim = h->S.dim;
+        g_kernel_p = h->S.p;
         if (use_v0()) {
             dev_local_solve(h->P, e, d, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
         } else {
             const int pr = e * h->S.nd + d;
             CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-            dev_gj_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+            if (kernel_choice() == 1)
+                dev_gj_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+            else
+                dev_dmma_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
         }
         CUDA_OK(cudaMemcpyAsync(out, h->d_vec2, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         check_err(h);
@@ -1889,7 +1914,12 @@ int hsw_fp64_peak(int device, double* tflops) {
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
             throw hsw::Error(HSW_ERR_CUDA, "hsw_fp64_peak: no CUDA device");
-        *tflops = dev_fp64_peak_tflops(device);
+        // the FP64 roofline: max of the CUDA-core DFMA and the tensor-core DMMA rates
+        const double dfma = dev_fp64_peak_tflops(device);
+        const double dmma = dev_dmma_peak_tflops(device);
+        if (const char* v = std::getenv("HSW_PEAK_VERBOSE"))
+            if (v[0] == '1') std::fprintf(stderr, "fp64 peak: DFMA %.2f TFLOP/s, DMMA %.2f TFLOP/s\n", dfma, dmma);
+        *tflops = dfma > dmma ? dfma : dmma;
         return HSW_OK;
     });
 }
@@ -1897,6 +1927,14 @@ int hsw_fp64_peak(int device, double* tflops) {
 int hsw_debug_flags(hsw_handle* h, int flags) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_flags: null handle");
     h->P.debug_flags = flags;
+    if (h->d_prof) cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long));
+    return HSW_OK;
+}
+
+int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]) {
+    if (!h || !h->d_prof) return fail(HSW_ERR_INVALID, "hsw_debug_profile: no device state");
+    cudaStreamSynchronize(h->stream);
+    cudaMemcpy(out, h->d_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return HSW_OK;
 }
 

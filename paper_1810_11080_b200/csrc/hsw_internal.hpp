@@ -41,7 +41,9 @@ struct DevProblem {
     const int* g_fidx;        // [6][128]
     const int* g_nmask;       // [128]
     const double* g_line;     // [8][8]
-    int debug_flags;          // ablation (tools/ablate.py): 1 skip faces, 2 skip elimination, 4 skip T loads
+    int debug_flags;          // ablation (tools/ablate.py): 1 skip faces, 2 skip elimination, 4 skip T loads,
+                              // 8 per-phase clock64 counters into prof[]
+    unsigned long long* prof; // [8] debug phase-cycle accumulators
 };
 
 // Host-computed tables that are uploaded to constant memory.
@@ -74,6 +76,7 @@ void dev_local_solve(const DevProblem& P, int e, int d, const double* rhs, doubl
                      unsigned long long* err_key, int64_t zero_pair, void* stream);
 int dev_max_dynamic_smem_needed(int dim, int p);
 double dev_fp64_peak_tflops(int device);
+double dev_dmma_peak_tflops(int device);
 // production register-resident Gauss-Jordan sweep (hsw_gj.cu)
 void dev_upload_gj_tables(const ConstTables& t, const int* fidx /*6*128*/, const double* line /*8*8*/);
 void dev_gj_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
@@ -81,5 +84,10 @@ void dev_gj_sweep(const DevProblem& P, const double* src, const double* psi_old,
 void dev_gj_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                         unsigned long long* err_key, int64_t zero_pair, void* stream);
 int dev_gj_smem(int dim, int p);
+// production blocked Gauss-Jordan with DMMA trailing updates (hsw_dmma.cu)
+void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
+                    const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
+void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
+                          unsigned long long* err_key, int64_t zero_pair, void* stream);
 
 }  // namespace hsw

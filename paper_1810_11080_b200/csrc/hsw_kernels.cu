@@ -443,6 +443,54 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, 
     if (r == 12345.678) out[0] = r;  // keep the chains alive
 }
 
+// FP64 tensor-core (DMMA m8n8k4) throughput: 8 independent accumulator tiles per warp
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i][0] = threadIdx.x * 1e-9 + i; c[i][1] = 0.0; }
+    const double a = 1e-3 + threadIdx.x * 1e-12, b = 0.999;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+    if (r == 12345.678) out[0] = r;
+}
+
+double dev_dmma_peak_tflops(int device) {
+    KCHECK(cudaSetDevice(device));
+    int sms = 0;
+    KCHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* out = nullptr;
+    KCHECK(cudaMalloc(&out, sizeof(double)));
+    const int blocks = sms * 8, threads = 256, iters = 2048;
+    dmma_peak_kernel<<<blocks, threads>>>(out, 16);
+    KCHECK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    KCHECK(cudaEventCreate(&e0));
+    KCHECK(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+        KCHECK(cudaEventRecord(e0));
+        dmma_peak_kernel<<<blocks, threads>>>(out, iters);
+        KCHECK(cudaEventRecord(e1));
+        KCHECK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        KCHECK(cudaEventElapsedTime(&ms, e0, e1));
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    // 8 DMMA (8x8x4 = 256 FMA = 512 FLOP) per warp per iteration
+    const double flops = 512.0 * 8.0 * (double)iters * (double)blocks * (threads / 32);
+    return flops / (best * 1e-3) * 1e-12;
+}
+
 double dev_fp64_peak_tflops(int device) {
     KCHECK(cudaSetDevice(device));
     int sms = 0;

@@ -8,9 +8,21 @@ P = pb.config(name)
 s = pk.SweepSolver(P)
 L = _capi.load()
 L.hsw_debug_flags.argtypes = [C.c_void_p, C.c_int]
-for flags in [0, 1, 2, 4, 3, 5, 6, 7]:
+for flags in ([0] if os.environ.get("QUICK") else [0, 1, 2, 4, 3, 5, 6, 7]):
     L.hsw_debug_flags(s.handle, flags)
     for _ in range(2):
         L.hsw_sweep_resident(s.handle); L.hsw_synchronize(s.handle)
     ms = L.hsw_last_sweep_kernel_ms(s.handle)
     print(f"{name} flags={flags} (1 no-faces, 2 no-elim, 4 no-T) sweep {ms:.2f} ms", flush=True)
+
+# per-phase clock64 counters (flag 8), cycles per pair as seen by one lane of the pair
+import numpy as np
+L.hsw_debug_profile.argtypes = [C.c_void_p, C.c_void_p]
+L.hsw_debug_flags(s.handle, 8)
+L.hsw_sweep_resident(s.handle); L.hsw_synchronize(s.handle)
+out = np.zeros(16, np.uint64)
+L.hsw_debug_profile(s.handle, C.c_void_p(out.ctypes.data))
+n = max(int(out[5]), 1)
+names = ["tables", "faces", "assembly", "elimination", "writeback"]
+print(name, "pairs", n, " ".join(f"{nm}={int(out[i])/n:.0f}cyc" for i, nm in enumerate(names)), flush=True)
+print(name, "panel loop:", " ".join(f"{nm}={int(out[8 + i])/n:.0f}cyc" for i, nm in enumerate(["wait", "U", "dmma", "factor"])), flush=True)
