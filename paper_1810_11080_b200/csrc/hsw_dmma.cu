@@ -369,6 +369,7 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
             }
         }
         double lr[RP][4];
+        int pst[4] = {-1, -1, -1, -1};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const int k = 4 * Pn + t;
@@ -411,11 +412,35 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
                 for (int i = 0; i < RP; ++i) pv[i][tt] -= lr[i][t] * u;
             }
             if (lane == (prow & 31)) rdone |= 1u << (prow >> 5);
+            pst[t] = prow;
             if (lane == 0) {
                 pivval[k] = piv;
                 rowstep[prow] = k;
                 prw[t] = prow;
             }
+        }
+        // L~ = L * L11^{-1}, L11[t2][t] = l_t(p_t2) (t < t2): then the trailing update is
+        // A -= L~ * A[P,:] with the raw pre-panel pivot rows as the B operand.
+        double l11[4][4];
+#pragma unroll
+        for (int t2 = 1; t2 < 4; ++t2)
+#pragma unroll
+            for (int t = 0; t < t2; ++t) {
+                const int p2 = pst[t2];
+                double v = lr[0][t];
+#pragma unroll
+                for (int i = 1; i < RP; ++i)
+                    if (p2 >= 0 && i == (p2 >> 5)) v = lr[i][t];
+                v = __shfl_sync(0xffffffffu, v, p2 >= 0 ? (p2 & 31) : 0);
+                l11[t2][t] = p2 >= 0 ? v : 0.0;
+            }
+#pragma unroll
+        for (int i = 0; i < RP; ++i) {
+            double lt3 = lr[i][3];
+            double lt2 = lr[i][2] - lt3 * l11[3][2];
+            double lt1 = lr[i][1] - lt2 * l11[2][1] - lt3 * l11[3][1];
+            double lt0 = lr[i][0] - lt1 * l11[1][0] - lt2 * l11[2][0] - lt3 * l11[3][0];
+            lr[i][0] = lt0; lr[i][1] = lt1; lr[i][2] = lt2; lr[i][3] = lt3;
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t)
@@ -468,56 +493,37 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
                 // every warp tracks the pivot set (the owner of a later panel searches with it)
                 if (pr4[t] >= 0 && lane == (pr4[t] & 31)) rdone |= 1u << (pr4[t] >> 5);
             }
-            // B fragments of U = L11^{-1} A[P,:] built with shuffles: lane (g, q) needs
-            // U[q][8j + g]; column 8j+g of pivot row p lives in lane ((p&7)<<2 | g>>1),
-            // slot g&1, tile-row p>>3 (uniform).  Zero on the panel's own columns.
-            double l10 = 0.0, l20 = 0.0, l21 = 0.0, l30 = 0.0, l31 = 0.0, l32 = 0.0;
-            if (pr4[1] >= 0) l10 = lpb[0 * NR + pr4[1]];
-            if (pr4[2] >= 0) { l20 = lpb[0 * NR + pr4[2]]; l21 = lpb[1 * NR + pr4[2]]; }
-            if (pr4[3] >= 0) { l30 = lpb[0 * NR + pr4[3]]; l31 = lpb[1 * NR + pr4[3]]; l32 = lpb[2 * NR + pr4[3]]; }
-            double bfr[TCW];
-            {
-                double ur[TCW][4];
+            // B fragments = raw pre-panel pivot rows over this warp's columns (L11^{-1} is
+            // folded into the published multipliers): the quad holding pivot row p_t
+            // writes it to SMEM, lane (g, q) reads B[q][8j + g].
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int p = pr4[t];
-                    const int tp = p >= 0 ? (p >> 3) : 0;
-                    const int src_l = ((p & 7) << 2) | (g >> 1);
-                    double v0[TCW], v1[TCW];
-                    switch (tp) {  // uniform: one branch, no select chains
-#define HSW_TP(T_)                                                                  \
-    case T_:                                                                        \
-        _Pragma("unroll") for (int j = 0; j < TCW; ++j) {                           \
-            v0[j] = acc[j][T_ < NTR ? T_ : 0][0];                                   \
-            v1[j] = acc[j][T_ < NTR ? T_ : 0][1];                                   \
-        }                                                                           \
+            for (int t = 0; t < 4; ++t) {
+                const int p = pr4[t];
+                if (p >= 0) {
+                    const bool holder = g == (p & 7);
+                    double* dst = Uraw + t * 8 * TCW + 2 * q;
+                    switch (p >> 3) {  // uniform tile-row of the pivot row
+#define HSW_TP(T_)                                                                            \
+    case T_:                                                                                  \
+        if (holder) {                                                                         \
+            _Pragma("unroll") for (int j = 0; j < TCW; ++j)                                   \
+                *reinterpret_cast<double2*>(dst + 8 * j) =                                    \
+                    make_double2(acc[j][T_ < NTR ? T_ : 0][0], acc[j][T_ < NTR ? T_ : 0][1]); \
+        }                                                                                     \
         break;
                         HSW_TP(0) HSW_TP(1) HSW_TP(2) HSW_TP(3) HSW_TP(4) HSW_TP(5) HSW_TP(6) HSW_TP(7)
                         HSW_TP(8) HSW_TP(9) HSW_TP(10) HSW_TP(11) HSW_TP(12) HSW_TP(13) HSW_TP(14) HSW_TP(15)
 #undef HSW_TP
-                        default:
-#pragma unroll
-                            for (int j = 0; j < TCW; ++j) v0[j] = v1[j] = 0.0;
-                            break;
-                    }
-#pragma unroll
-                    for (int j = 0; j < TCW; ++j) {
-                        const double s0 = __shfl_sync(0xffffffffu, v0[j], src_l);
-                        const double s1 = __shfl_sync(0xffffffffu, v1[j], src_l);
-                        ur[j][t] = p >= 0 ? ((g & 1) ? s1 : s0) : 0.0;
+                        default: break;
                     }
                 }
+            }
+            __syncwarp();
+            double bfr[TCW];
+            {
+                const bool qv = pr4[q] >= 0;
 #pragma unroll
-                for (int j = 0; j < TCW; ++j) {
-                    const double u0 = ur[j][0];
-                    const double u1 = ur[j][1] - l10 * u0;
-                    const double u2 = ur[j][2] - l20 * u0 - l21 * u1;
-                    const double u3 = ur[j][3] - l30 * u0 - l31 * u1 - l32 * u2;
-                    const double mine = q == 0 ? u0 : (q == 1 ? u1 : (q == 2 ? u2 : u3));
-                    const int cglob = 8 * (j * W + w) + g;
-                    const bool own_cols = cglob >= 4 * Pn && cglob < 4 * Pn + 4 && cglob < N;  // never the rhs
-                    bfr[j] = own_cols ? 0.0 : mine;
-                }
+                for (int j = 0; j < TCW; ++j) bfr[j] = qv ? Uraw[q * 8 * TCW + 8 * j + g] : 0.0;
             }
             // lookahead: the owner of panel Pn+1 updates that tile-column first and factors it
             const int Pn1 = Pn + 1;
@@ -538,6 +544,7 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
                 const bool live = 8 * tcg + 7 >= 4 * Pn + 4 || tcg == N / 8;  // the rhs tile stays live
                 if (live && !(look && j == jn)) update_tc(j, lpb, bfr);
             }
+            __syncwarp();  // Uraw reuse by the next panel's gather
             c_mma += clock64() - c1;
             c0 = clock64();
             if (W > 1 && (Pn & 1)) pair_sync();  // bounds the 4-deep multiplier ring
