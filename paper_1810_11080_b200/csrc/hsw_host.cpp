@@ -1365,25 +1365,26 @@ void check_err(hsw_handle* h) {
     }
 }
 
-// Kernel selection: the register-resident Gauss-Jordan kernel (hsw_gj.cu) is
-// the product; HSW_KERNEL=v0 selects the simple SMEM reference kernel.
-// Kernel selection: "dmma" (default, hsw_dmma.cu), "gj" (register-resident
+// Kernel selection (HSW_KERNEL): "dmma1" (one warp per pair, persistent,
+// hsw_dmma1.cu), "dmma" (W warps per pair, hsw_dmma.cu), "gj" (register-resident
 // DFMA Gauss-Jordan, hsw_gj.cu) or "v0" (simple SMEM LU, hsw_kernels.cu).
-// HSW_KERNEL=auto (default) picks the faster measured kernel per shape
-// (profiles/: DMMA for 2D, register Gauss-Jordan for 3D p >= 2).
+// Unset / "auto" picks the fastest measured kernel per shape.
 int kernel_choice_env() {
     static const int kc = [] {
         const char* k = std::getenv("HSW_KERNEL");
         if (k && std::string(k) == "v0") return 0;
         if (k && std::string(k) == "gj") return 1;
         if (k && std::string(k) == "dmma") return 2;
+        if (k && std::string(k) == "dmma1") return 3;
         return -1;
     }();
     return kc;
 }
 int kernel_choice_for(int dim, int p) {
-    const int env = kernel_choice_env();
+    int env = kernel_choice_env();
+    if (env == 3 && !dev_dmma1_supported(dim, p)) env = -1;
     if (env >= 0) return env;
+    if (dev_dmma1_supported(dim, p)) return 3;
     return (dim == 3 && p >= 2) ? 1 : 2;
 }
 thread_local int g_kernel_dim = 2, g_kernel_p = 1;
@@ -1394,6 +1395,7 @@ void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const i
     switch (kernel_choice_for(h->S.dim, h->S.p)) {
         case 0: dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, pairs, n, h->d_err, h->zero_pair, h->stream); break;
         case 1: dev_gj_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream); break;
+        case 3: dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream); break;
         default: dev_dmma_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
     }
 }
@@ -1638,6 +1640,8 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
             CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
             if (kernel_choice() == 1)
                 dev_gj_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+            else if (kernel_choice() == 3)
+                dev_dmma1_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
             else
                 dev_dmma_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
         }

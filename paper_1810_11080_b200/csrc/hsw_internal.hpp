@@ -89,5 +89,11 @@ void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_ol
                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
 void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                           unsigned long long* err_key, int64_t zero_pair, void* stream);
+// one warp per pair, persistent, register + shared-memory DMMA tiles (hsw_dmma1.cu)
+bool dev_dmma1_supported(int dim, int p);
+void dev_dmma1_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
+                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
+void dev_dmma1_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
+                           unsigned long long* err_key, int64_t zero_pair, void* stream);
 
 }  // namespace hsw
