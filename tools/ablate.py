@@ -25,4 +25,4 @@ L.hsw_debug_profile(s.handle, C.c_void_p(out.ctypes.data))
 n = max(int(out[5]), 1)
 names = ["tables", "faces", "assembly", "elimination", "writeback"]
 print(name, "pairs", n, " ".join(f"{nm}={int(out[i])/n:.0f}cyc" for i, nm in enumerate(names)), flush=True)
-print(name, "panel loop:", " ".join(f"{nm}={int(out[8 + i])/n:.0f}cyc" for i, nm in enumerate(["wait", "U", "dmma", "factor"])), flush=True)
+print(name, "panel loop:", " ".join(f"{nm}={int(out[8 + i])/n:.0f}cyc" for i, nm in enumerate([os.environ.get("P8", "wait"), os.environ.get("P9", "U"), "dmma", "factor"])), flush=True)
