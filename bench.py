@@ -13,7 +13,7 @@ source rebuilt from the resident phi.  Inputs (psi, 2 x 4.3 GB at C4) exceed the
   e2e        same metric through the reference-facing C ABI call hsw_sweep(d=-1)
              with pinned HOST buffers: H2D psi_old+phi and D2H psi_new inside
              the timed region
-  roofline   dominant kernel (the Gauss-Jordan sweep kernel): LU-algorithmic
+  roofline   dominant kernel (the sweep kernel, one launch per level): LU-algorithmic
              FP64 FLOPs F(n) = 2/3 n^3 + 2 n^2 per solve / kernel time, against
              the FP64 peak measured in-run (DFMA microbenchmark)
   cpu_baseline  the CPU oracle (port of the reference algorithm) on the host
@@ -284,7 +284,11 @@ def run_ours(args):
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            tj = json.load(open(prof))
+            if "dram_bytes_per_pair" in tj:   # ncu capture of one level, scaled to the average launch
+                traffic = tj["dram_bytes_per_pair"] * pairs / max(launches_per_step - 1, 1)
+            else:
+                traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
