@@ -20,7 +20,11 @@ source rebuilt from the resident phi.  Inputs (psi, 2 x 4.3 GB at C4) exceed the
              cores, bounded sample of the same workload
 --impl reference times the CPU oracle port alone (the reference itself cannot
 be built here: Eigen/Catch2/CLI11 are absent) on the same config/metric.
-Multi-GPU (N > 1): independent replicas of the full sweep per rank ("weak").
+Multi-GPU (N > 1): the ordinates are sharded over the ranks
+(paper_1810_11080_b200/sharded.py); one step = every rank sweeps its ordinate
+block and phi is formed by the chained prefix in ordinate order + broadcast over
+NCCL (bit-identical to one GPU).  value = all pairs / max-over-ranks step time
+("strong" scaling: the job is fixed).  --sharded forces this path at N = 1.
 """
 from __future__ import annotations
 
@@ -49,6 +53,14 @@ UNIT = "solves/s"
 
 def flops_per_solve(n: int) -> float:
     return 2.0 / 3.0 * n ** 3 + 2.0 * n * n
+
+
+class _DevView:
+    """Raw device pointer as a torch-importable array (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
 
 
 def dist_env():
@@ -210,10 +222,37 @@ def run_ours(args):
     assert L.hsw_set_state(h, C.c_void_p(phi0.ctypes.data), None) == 0, _capi.last_error()
     torch.cuda.synchronize()
 
+    sharded = world > 1 or args.sharded
+    if sharded:
+        from paper_1810_11080_b200.sharded import DeviceShardBackend, block_of
+        be = DeviceShardBackend(solver)
+        d0, d1 = block_of(prob.num_ordinates, rank, world)
+        phi_t = torch.full((prob.num_dofs,), 0.1, dtype=torch.float64, device=f"cuda:{local}")
+
+        def step():
+            # one source-iteration data path: block sweep + chained phi (sharded.py)
+            be.sweep(d0, d1, phi_t)
+            prefix = None
+            if world > 1 and rank > 0:
+                prefix = be.zeros()
+                torch.distributed.recv(prefix, src=rank - 1)
+            out = be.zeros()
+            be.phi_partial(d0, d1, prefix, out)
+            if world > 1:
+                if rank < world - 1:
+                    torch.distributed.send(out, dst=rank + 1)
+                torch.distributed.broadcast(out, src=world - 1)
+            return L.hsw_last_launch_count(h) + 1
+    else:
+        def step():
+            rc = L.hsw_sweep_resident(h)
+            assert rc == 0, _capi.last_error()
+            return L.hsw_last_launch_count(h)
+
     for _ in range(args.warmup):
-        assert L.hsw_sweep_resident(h) == 0
-        assert L.hsw_synchronize(h) == 0
-    launches_per_step = L.hsw_last_launch_count(h)
+        step()
+        assert L.hsw_synchronize(h) == 0, _capi.last_error()
+    torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -221,15 +260,13 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     kernel_ms = []
-    with torch.cuda.stream(stream):
-        ev0.record(stream)
-        for _ in range(args.steps):
-            rc = L.hsw_sweep_resident(h)
-            assert rc == 0, _capi.last_error()
-            # the per-sweep kernel time (events around the level launches) is read
-            # after the region; synchronising here would not change device time
-            ev_mid = None
-        ev1.record(stream)
+    launches_per_step = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        launches_per_step = step()
+    if sharded:   # the last broadcast runs on torch's stream: close the span after it
+        torch.cuda.current_stream().synchronize()
+    ev1.record(stream)
     torch.cuda.synchronize()
     rc = L.hsw_synchronize(h)
     assert rc == 0, _capi.last_error()
@@ -238,55 +275,95 @@ def run_ours(args):
     ms_total = ev0.elapsed_time(ev1)
     # kernel-only time of one sweep (events around the sweep-kernel launches)
     for _ in range(2):
-        L.hsw_sweep_resident(h)
+        if sharded:
+            be.sweep(d0, d1, phi_t)
+        else:
+            L.hsw_sweep_resident(h)
         L.hsw_synchronize(h)
         kernel_ms.append(L.hsw_last_sweep_kernel_ms(h))
     kms = min(kernel_ms)
     ms_step = ms_total / args.steps
     if world > 1:
-        t = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms_step, kms], dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = world * pairs / (ms_step * 1e-3)
+        ms_step, kms = float(t[0].item()), float(t[1].item())
+    value = pairs / (ms_step * 1e-3)
 
     # ---- end-to-end through the reference-facing ABI call with pinned host buffers
     e2e = None
     if not args.skip_e2e:
         N = prob.num_dofs
         nd = prob.num_ordinates
-        phi_h = torch.full((N,), 0.1, dtype=torch.float64).pin_memory()
-        psi_old_h = torch.zeros((nd, N), dtype=torch.float64).pin_memory()
-        psi_new_h = torch.empty((nd, N), dtype=torch.float64).pin_memory()
         vp = C.c_void_p
-        for _ in range(1):
-            assert L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr())) == 0
-        e2e_steps = max(1, min(args.steps, 3))
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            rc = L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr()))
-            assert rc == 0, _capi.last_error()
-            psi_old_h, psi_new_h = psi_new_h, psi_old_h
-        barrier()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if sharded:
+            # per rank: H2D of its psi_old block + phi, block sweep + phi chain, D2H of its psi_new block
+            pa, pb_, ph = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            assert L.hsw_device_state(h, C.byref(pa), C.byref(pb_), C.byref(ph)) == 0
+            nb = d1 - d0
+            phi_h = torch.full((N,), 0.1, dtype=torch.float64).pin_memory()
+            psi_old_h = torch.zeros((nb, N), dtype=torch.float64).pin_memory()
+            psi_new_h = torch.empty((nb, N), dtype=torch.float64).pin_memory()
+            vp = C.c_void_p
+
+            def e2e_step():
+                cu = torch.cuda.current_stream()
+                pa2, pb2, ph2 = C.c_void_p(), C.c_void_p(), C.c_void_p()
+                L.hsw_device_state(h, C.byref(pa2), C.byref(pb2), C.byref(ph2))
+                dev_old = _DevView(pa2.value + d0 * N * 8, (nb, N))
+                torch.as_tensor(dev_old, device=f"cuda:{local}").copy_(psi_old_h, non_blocking=True)
+                phi_t.copy_(phi_h, non_blocking=True)
+                cu.synchronize()
+                step()
+                L.hsw_synchronize(h)
+                dev_new = _DevView(pb2.value + d0 * N * 8, (nb, N))
+                psi_new_h.copy_(torch.as_tensor(dev_new, device=f"cuda:{local}"), non_blocking=True)
+                cu.synchronize()
+
+            e2e_step()
+            e2e_steps = max(1, min(args.steps, 3))
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                e2e_step()
+            barrier()
+            e2e_s = (time.perf_counter() - t0) / e2e_steps
+            h2d, d2h = (nd * N + world * N) * 8, nd * N * 8
+            api = "per rank: psi_old block + phi H2D, hsw_shard_sweep + chained phi (NCCL), psi_new block D2H"
+        else:
+            phi_h = torch.full((N,), 0.1, dtype=torch.float64).pin_memory()
+            psi_old_h = torch.zeros((nd, N), dtype=torch.float64).pin_memory()
+            psi_new_h = torch.empty((nd, N), dtype=torch.float64).pin_memory()
+            for _ in range(1):
+                assert L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr())) == 0
+            e2e_steps = max(1, min(args.steps, 3))
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                rc = L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr()))
+                assert rc == 0, _capi.last_error()
+                psi_old_h, psi_new_h = psi_new_h, psi_old_h
+            barrier()
+            e2e_s = (time.perf_counter() - t0) / e2e_steps
+            h2d, d2h = (nd * N + N) * 8, nd * N * 8
+            api = "hsw_sweep(h, -1, phi, psi_old, psi_new) host pointers"
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": world * pairs / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": (nd * N + N) * 8, "d2h_bytes_per_step": nd * N * 8,
-               "ms_per_step": e2e_s * 1e3, "api": "hsw_sweep(h, -1, phi, psi_old, psi_new) host pointers"}
+        e2e = {"value": pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_s * 1e3, "api": api}
         del phi_h, psi_old_h, psi_new_h
 
     # ---- roofline of the dominant kernel (the sweep kernel)
-    achieved = flops_per_solve(n) * pairs / (kms * 1e-3) * 1e-12
+    pairs_rank = pairs if not sharded else prob.num_elements * (d1 - d0)
+    achieved = flops_per_solve(n) * pairs_rank / (kms * 1e-3) * 1e-12
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
             if "dram_bytes_per_pair" in tj:   # ncu capture of one level, scaled to the average launch
-                traffic = tj["dram_bytes_per_pair"] * pairs / max(launches_per_step - 1, 1)
+                traffic = tj["dram_bytes_per_pair"] * pairs_rank / max(launches_per_step - 1, 1)
             else:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
@@ -310,12 +387,14 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong",   # total work fixed as N grows (ordinates sharded over ranks)
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json configs, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_TEXT[args.config]}", "pairs": pairs, "n": n,
                        "levels": solver.num_levels, "l2": "inputs larger than L2 (psi 2 x "
                        f"{prob.num_ordinates * prob.num_dofs * 8 / 1e9:.2f} GB)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"ordinate-sharded x{world}: block [{d0}, {d1}) on rank 0, chained phi over "
+                                       f"{'NCCL' if world > 1 else 'one rank'}") if sharded else "1 GPU",
                        "setup_s": round(setup_s, 2)},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": int(launches_per_step * args.steps),
@@ -337,6 +416,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="ordinate-sharded step even at N = 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -198,6 +198,36 @@ int64_t hsw_last_launch_count(const hsw_handle* h);
  * hsw_sweep_resident call, measured with CUDA events on the handle's stream. */
 double hsw_last_sweep_kernel_ms(const hsw_handle* h);
 
+/* ---- direction-sharded source iteration ----------------------
+ * source_iteration's sweeps are independent per ordinate (solver.hpp:145-149),
+ * so a rank owns an ordinate block [d0, d1) and exchanges only phi.  These are
+ * the per-rank device primitives; the collective driver is
+ * paper_1810_11080_b200/sharded.py.  Pointers named *_dev are DEVICE pointers on
+ * the handle's device; all work is ordered on hsw_stream(h), no host sync unless
+ * a host output is returned.  HSW_ERR_RANGE unless 0 <= d0 < d1 <= nd. */
+/* psi_old = psi_new = 0 for every ordinate, resident phi = 0 (solver.hpp:139-141). */
+int hsw_shard_reset(hsw_handle* h);
+/* Scattering source from phi_dev (NULL: the resident phi), then sweep the
+ * ordinates [d0, d1): psi_new from the resident psi_old (lagged couplings) and
+ * the block's own retained upwind values.  Worklist: the block's pairs sorted
+ * by (level, element, ordinate), built once per block and cached. */
+int hsw_shard_sweep(hsw_handle* h, int d0, int d1, const double* phi_dev);
+/* out_dev = prefix_dev + sum_{d0 <= d < d1} w_d psi_new_d, accumulated per
+ * (e, m) in ascending d with one FMA per ordinate (prefix_dev NULL: 0).
+ * Chaining blocks in rank order reproduces hsw_source_iteration's phi bit for
+ * bit (solver.hpp:157-158). */
+int hsw_shard_phi_partial(hsw_handle* h, int d0, int d1, const double* prefix_dev, double* out_dev);
+/* *err = max over d in [d0, d1) of ||psi_new_d - psi_old_d||_inf (solver.hpp:150-156). */
+int hsw_shard_psi_error(hsw_handle* h, int d0, int d1, double* err);
+/* out2 = { sum (phi_new - phi_old)^2, sum phi_new^2 } with the same fixed-shape
+ * reduction tree as hsw_source_iteration (identical bits for identical phi). */
+int hsw_shard_phi_norms(hsw_handle* h, const double* phi_new_dev, const double* phi_old_dev, double out2[2]);
+/* psi_old <- psi_new (buffer swap) and resident phi <- phi_dev (NULL: keep). */
+int hsw_shard_advance(hsw_handle* h, const double* phi_dev);
+/* Copy psi_old (the latest completed iterate) of ordinates [d0, d1) to host
+ * psi ((d1-d0)*N doubles, ordinate-major). */
+int hsw_shard_psi(hsw_handle* h, int d0, int d1, double* psi);
+
 /* Measured FP64 FMA throughput of the device (TFLOP/s) from a DFMA-chain
  * microbenchmark over all SMs (~0.1 s); the roofline denominator of the
  * sweep kernel.  device: CUDA ordinal. */

@@ -1301,6 +1301,12 @@ struct hsw_handle {
     int64_t last_launches = 0;
     double last_kernel_ms = 0.0;
     size_t N = 0;
+    // direction-sharded SI: cached worklists of ordinate blocks [d0, d1)
+    struct RangeList {
+        int* d_pairs = nullptr;
+        std::vector<int> offsets;   // num_levels + 1
+    };
+    std::map<std::pair<int, int>, RangeList> ranges;
 };
 
 namespace {
@@ -1336,6 +1342,8 @@ void free_handle(hsw_handle* h) {
                     h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    for (auto& kv : h->ranges)
+        if (kv.second.d_pairs) cudaFree(kv.second.d_pairs);
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1412,6 +1420,44 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
         ++launches;
     }
     if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+    h->last_launches = launches;
+}
+
+// Worklist of the ordinate block [d0, d1): the all-ordinate list filtered,
+// so the (level, element, ordinate) order and every pair's inputs are unchanged.
+const hsw_handle::RangeList& range_list(hsw_handle* h, int d0, int d1) {
+    auto key = std::make_pair(d0, d1);
+    auto it = h->ranges.find(key);
+    if (it != h->ranges.end()) return it->second;
+    const auto& off = h->S.level_offsets;
+    const int nd = h->S.nd;
+    std::vector<int> pairs;
+    hsw_handle::RangeList rl;
+    rl.offsets.assign(off.size(), 0);
+    for (size_t l = 0; l + 1 < off.size(); ++l) {
+        for (int i = off[l]; i < off[l + 1]; ++i) {
+            const int d = h->S.pairs_all[i] % nd;
+            if (d >= d0 && d < d1) pairs.push_back(h->S.pairs_all[i]);
+        }
+        rl.offsets[l + 1] = (int)pairs.size();
+    }
+    if (!pairs.empty()) {
+        CUDA_OK(cudaMalloc(&rl.d_pairs, pairs.size() * sizeof(int)));
+        CUDA_OK(cudaMemcpy(rl.d_pairs, pairs.data(), pairs.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    return h->ranges.emplace(key, std::move(rl)).first->second;
+}
+
+void run_range_levels(hsw_handle* h, const hsw_handle::RangeList& rl, const double* psi_old, double* psi_new) {
+    CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launches = 0;
+    for (size_t l = 0; l + 1 < rl.offsets.size(); ++l) {
+        const int n = rl.offsets[l + 1] - rl.offsets[l];
+        if (n == 0) continue;
+        sweep_launch(h, psi_old, psi_new, rl.d_pairs + rl.offsets[l], n);
+        ++launches;
+    }
+    CUDA_OK(cudaEventRecord(h->ev1, h->stream));
     h->last_launches = launches;
 }
 
@@ -1891,6 +1937,103 @@ int hsw_sweep_resident(hsw_handle* h) {
         dev_scatter_source(h->P, h->d_phi, h->d_src, h->stream);
         run_all_levels(h, h->d_psiA, h->d_psiB, true);
         h->last_launches += 1;  // scatter-source kernel
+        return HSW_OK;
+    });
+}
+
+// ---- direction-sharded source iteration primitives
+namespace {
+void check_block(const hsw_handle* h, int d0, int d1, const char* what) {
+    if (d0 < 0 || d1 > h->S.nd || d0 >= d1)
+        throw hsw::Error(HSW_ERR_RANGE, std::string(what) + ": ordinate block [" + std::to_string(d0) + ", " +
+                                            std::to_string(d1) + ") out of range");
+}
+}  // namespace
+
+int hsw_shard_reset(hsw_handle* h) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_reset: null handle");
+        need_device(h);
+        const size_t N = h->N, nd = (size_t)h->S.nd;
+        CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
+        CUDA_OK(cudaMemsetAsync(h->d_psiB, 0, N * nd * sizeof(double), h->stream));
+        CUDA_OK(cudaMemsetAsync(h->d_phi, 0, N * sizeof(double), h->stream));
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_sweep(hsw_handle* h, int d0, int d1, const double* phi_dev) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_sweep: null handle");
+        need_device(h);
+        check_block(h, d0, d1, "hsw_shard_sweep");
+        const auto& rl = range_list(h, d0, d1);
+        dev_scatter_source(h->P, phi_dev ? phi_dev : h->d_phi, h->d_src, h->stream);
+        run_range_levels(h, rl, h->d_psiA, h->d_psiB);
+        h->last_launches += 1;   // scatter-source kernel
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_phi_partial(hsw_handle* h, int d0, int d1, const double* prefix_dev, double* out_dev) {
+    return guarded([&] {
+        if (!h || !out_dev) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_phi_partial: null argument");
+        need_device(h);
+        check_block(h, d0, d1, "hsw_shard_phi_partial");
+        dev_phi_partial(h->P, h->d_psiB, d0, d1, prefix_dev, out_dev, h->stream);
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_psi_error(hsw_handle* h, int d0, int d1, double* err) {
+    return guarded([&] {
+        if (!h || !err) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_psi_error: null argument");
+        need_device(h);
+        check_block(h, d0, d1, "hsw_shard_psi_error");
+        const size_t N = h->N;
+        dev_max_abs_diff(h->d_psiB + (size_t)d0 * N, h->d_psiA + (size_t)d0 * N, (int64_t)((size_t)(d1 - d0) * N),
+                         h->d_scratch, h->d_out, h->stream);
+        CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        check_err(h);   // synchronises; raises a singular local block of this sweep
+        *err = h->h_out[0];
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_phi_norms(hsw_handle* h, const double* phi_new_dev, const double* phi_old_dev, double out2[2]) {
+    return guarded([&] {
+        if (!h || !phi_new_dev || !phi_old_dev || !out2)
+            throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_phi_norms: null argument");
+        need_device(h);
+        dev_phi_norms2(h->P, phi_new_dev, phi_old_dev, h->d_scratch, h->d_out, h->stream);
+        CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        out2[0] = h->h_out[1];
+        out2[1] = h->h_out[2];
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_advance(hsw_handle* h, const double* phi_dev) {
+    return guarded([&] {
+        if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_advance: null handle");
+        need_device(h);
+        std::swap(h->d_psiA, h->d_psiB);
+        if (phi_dev)
+            CUDA_OK(cudaMemcpyAsync(h->d_phi, phi_dev, h->N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_psi(hsw_handle* h, int d0, int d1, double* psi) {
+    return guarded([&] {
+        if (!h || !psi) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_psi: null argument");
+        need_device(h);
+        check_block(h, d0, d1, "hsw_shard_psi");
+        const size_t N = h->N;
+        CUDA_OK(cudaMemcpyAsync(psi, h->d_psiA + (size_t)d0 * N, (size_t)(d1 - d0) * N * sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
         return HSW_OK;
     });
 }

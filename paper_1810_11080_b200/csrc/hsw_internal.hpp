@@ -89,6 +89,11 @@ void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_ol
                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
 void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                           unsigned long long* err_key, int64_t zero_pair, void* stream);
+// direction-sharded source iteration (hsw_kernels.cu)
+void dev_phi_partial(const DevProblem& P, const double* psi_new, int d0, int d1, const double* prefix, double* out,
+                     void* stream);
+void dev_phi_norms2(const DevProblem& P, const double* phi_new, const double* phi_old, double* scratch, double* out3,
+                    void* stream);
 // one warp per pair, persistent, register + shared-memory DMMA tiles (hsw_dmma1.cu)
 bool dev_dmma1_supported(int dim, int p);
 void dev_dmma1_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,

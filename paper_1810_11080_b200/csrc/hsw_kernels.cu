@@ -348,13 +348,13 @@ phi_norms_kernel(const DevProblem pr, const double* __restrict__ psi_new, const 
         double ph = 0.0;
         for (int d = 0; d < pr.nd; ++d) {
             const double a = psi_new[(size_t)d * N + i];
-            ph += pr.weight[d] * a;
+            ph = fma(pr.weight[d], a, ph);   // explicit: hsw_shard_phi_partial chains the same FMAs
             mx = fmax(mx, fabs(a - psi_old[(size_t)d * N + i]));
         }
         phi_new[i] = ph;
         const double df = ph - phi_old[i];
-        num += df * df;
-        den += ph * ph;
+        num = fma(df, df, num);
+        den = fma(ph, ph, den);
     }
     __shared__ double s0[kRedThreads], s1[kRedThreads], s2[kRedThreads];
     s0[threadIdx.x] = mx; s1[threadIdx.x] = num; s2[threadIdx.x] = den;
@@ -518,6 +518,66 @@ double dev_fp64_peak_tflops(int device) {
     cudaFree(out);
     const double flops = 2.0 * 8.0 * 16.0 * (double)iters * (double)blocks * threads;
     return flops / (best * 1e-3) * 1e-12;
+}
+
+// ----------------------------------------------- direction-sharded SI (§8e)
+// out = prefix + sum_{d0 <= d < d1} w_d psi_new_d with the FMA chain of
+// phi_norms_kernel: chaining the blocks of all ranks in order gives its bits.
+__global__ void phi_partial_kernel(const DevProblem pr, const double* __restrict__ psi_new, int d0, int d1,
+                                   const double* __restrict__ prefix, double* __restrict__ out) {
+    const int64_t N = (int64_t)pr.nel * pr.nb;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        double ph = prefix ? prefix[i] : 0.0;
+        for (int d = d0; d < d1; ++d) ph = fma(pr.weight[d], psi_new[(size_t)d * N + i], ph);
+        out[i] = ph;
+    }
+}
+
+void dev_phi_partial(const DevProblem& P, const double* psi_new, int d0, int d1, const double* prefix, double* out,
+                     void* stream) {
+    const int64_t N = (int64_t)P.nel * P.nb;
+    const int nblk = (int)std::min<int64_t>(4096, (N + 255) / 256);
+    phi_partial_kernel<<<nblk, 256, 0, (cudaStream_t)stream>>>(P, psi_new, d0, d1, prefix, out);
+    KCHECK(cudaGetLastError());
+}
+
+// sum (phi_new - phi_old)^2 and sum phi_new^2 with phi_norms_kernel's exact tree
+__global__ void __launch_bounds__(kRedThreads)
+phi_norms2_kernel(int64_t N, const double* __restrict__ phi_new, const double* __restrict__ phi_old,
+                  double* __restrict__ part) {
+    double num = 0.0, den = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < N; i += (int64_t)gridDim.x * kRedThreads) {
+        const double ph = phi_new[i];
+        const double df = ph - phi_old[i];
+        num = fma(df, df, num);
+        den = fma(ph, ph, den);
+    }
+    __shared__ double s1[kRedThreads], s2[kRedThreads];
+    s1[threadIdx.x] = num; s2[threadIdx.x] = den;
+    __syncthreads();
+    for (int off = kRedThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            s1[threadIdx.x] += s1[threadIdx.x + off];
+            s2[threadIdx.x] += s2[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = 0.0;
+        part[gridDim.x + blockIdx.x] = s1[0];
+        part[2 * gridDim.x + blockIdx.x] = s2[0];
+    }
+}
+
+void dev_phi_norms2(const DevProblem& P, const double* phi_new, const double* phi_old, double* scratch, double* out3,
+                    void* stream) {
+    const int64_t N = (int64_t)P.nel * P.nb;
+    const int nblk = (int)std::min<int64_t>(kRedBlocks, (N + kRedThreads - 1) / kRedThreads);
+    cudaStream_t st = (cudaStream_t)stream;
+    phi_norms2_kernel<<<nblk, kRedThreads, 0, st>>>(N, phi_new, phi_old, scratch);
+    KCHECK(cudaGetLastError());
+    finish3_kernel<<<1, kRedThreads, 0, st>>>(scratch, nblk, out3);
+    KCHECK(cudaGetLastError());
 }
 
 void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scratch, double* out, void* stream) {

@@ -150,6 +150,7 @@ class SweepSolver:
         L = _capi.load()
         self.problem = problem
         self._options = options or SolveOptions()
+        self.device = device
         keep = []
 
         def arr(a, dt):

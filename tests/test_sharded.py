@@ -1,0 +1,121 @@
+"""Direction-sharded source iteration: host logic and collectives.
+
+CPU (gloo, world_size 2) with the oracle-backed test backend; GPU parity of the
+device primitives against hsw_source_iteration in test_sharded_gpu below.
+"""
+import os
+import sys
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1810_11080_b200 import problem as pb
+from paper_1810_11080_b200.sharded import block_of, sharded_source_iteration
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _oracle_shard_backend import OracleShardBackend  # noqa: E402
+
+PROB = dict(name="c1", cells=3, n_mu=2, n_az=4)   # 9 elements, 8 ordinates, Q2
+
+
+def _problem():
+    kw = dict(PROB)
+    return pb.config(kw.pop("name"), **kw)
+
+
+def test_blocks_partition_the_ordinates():
+    for nd in (1, 7, 8, 256):
+        for world in range(1, min(nd, 9) + 1):
+            blocks = [block_of(nd, r, world) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == nd
+            assert all(b[0] == a[1] for a, b in zip(blocks, blocks[1:]))
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+    with pytest.raises(ValueError):
+        block_of(4, 0, 5)
+    with pytest.raises(ValueError):
+        block_of(4, 4, 4)
+
+
+def test_one_rank_reproduces_the_oracle_source_iteration():
+    prob = _problem()
+    be = OracleShardBackend(prob)
+    res = sharded_source_iteration(be, tolerance=1e-10, max_iterations=200, criterion="phi_rel_l2",
+                                   return_psi=True)
+    ref = be.o.source_iteration(1e-10, 200, 1)
+    assert res.converged and ref["converged"]
+    assert res.iterations == ref["iterations"]
+    assert np.array_equal(res.phi, ref["phi"])
+    assert np.array_equal(res.psi, ref["psi"])
+    assert res.errors == list(ref["error"]) and res.phi_rels == list(ref["phi_rel"])
+
+
+def test_local_blocks_are_bit_identical_to_one_block():
+    prob = _problem()
+    one = sharded_source_iteration(OracleShardBackend(prob), tolerance=1e-9, criterion="psi_linf",
+                                   return_psi=True)
+    three = sharded_source_iteration(OracleShardBackend(prob), tolerance=1e-9, criterion="psi_linf",
+                                     local_blocks=3, return_psi=True)
+    assert three.blocks == [(0, 2), (2, 5), (5, 8)]
+    assert one.iterations == three.iterations
+    assert np.array_equal(one.phi, three.phi) and np.array_equal(one.psi, three.psi)
+    assert one.errors == three.errors
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, outdir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        res = sharded_source_iteration(OracleShardBackend(_problem()), tolerance=1e-10, max_iterations=200,
+                                       criterion="phi_rel_l2", return_psi=True)
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), phi=res.phi, psi=res.psi, blocks=np.array(res.blocks),
+                 it=res.iterations, conv=res.converged, errs=np.array(res.errors), rels=np.array(res.phi_rels))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_match_one_rank_bit_for_bit(world):
+    prob = _problem()
+    ref = sharded_source_iteration(OracleShardBackend(prob), tolerance=1e-10, max_iterations=200,
+                                   criterion="phi_rel_l2", return_psi=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_worker, args=(world, _free_port(), tmp), nprocs=world, join=True)
+        outs = [np.load(os.path.join(tmp, f"r{r}.npz")) for r in range(world)]
+    psi = np.concatenate([o["psi"] for o in outs])
+    for r, o in enumerate(outs):
+        assert tuple(o["blocks"][0]) == block_of(prob.num_ordinates, r, world)
+        assert int(o["it"]) == ref.iterations and bool(o["conv"])
+        assert np.array_equal(o["phi"], ref.phi)            # chained prefix: identical bits on every rank
+        assert list(o["errs"]) == ref.errors and list(o["rels"]) == ref.phi_rels
+    assert np.array_equal(psi, ref.psi)
+
+
+@pytest.mark.gpu
+def test_device_shards_match_hsw_source_iteration_bit_for_bit():
+    """The hsw_shard_* primitives (range worklists, chained FMA phi, norm tree)
+    reproduce the single-device source iteration exactly, for 1 and 4 blocks."""
+    import paper_1810_11080_b200 as pk
+    from paper_1810_11080_b200.sharded import DeviceShardBackend
+    for name, kw in (("c1", {}), ("c3", dict(cells=4, n_mu=2, n_az=4))):
+        prob = pb.config(name, **kw)
+        s = pk.SweepSolver(prob, pk.SolveOptions(tolerance=1e-8, criterion="phi_rel_l2"))
+        state, hist = s.source_iteration()
+        for blocks in (None, 4):
+            res = sharded_source_iteration(DeviceShardBackend(s), tolerance=1e-8, criterion="phi_rel_l2",
+                                           local_blocks=blocks, return_psi=True)
+            assert res.converged and hist.converged
+            assert res.iterations == hist.iterations()
+            assert np.array_equal(res.phi, state.phi)
+            assert np.array_equal(res.psi, state.psi)
+            assert res.errors == list(hist.error) and res.phi_rels == list(hist.phi_rel)
