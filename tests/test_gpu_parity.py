@@ -145,3 +145,27 @@ def test_full_config_sampled_ordinates(name):
         so = gpu.ordering(d)
         assert (so.order == oo["order"]).all() and (so.lagged_edges == oo["lagged_edges"]).all()
         assert (so.level == oo["level"]).all()
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_singular_block_3d_production_kernels(name):
+    """A zeroed local block is reported with its (element, ordinate) by each 3D
+    production kernel (c3: one-warp DMMA, c4: DMMA with TMEM tiles, c5: register GJ)."""
+    prob = pb.config(name, cells=2, n_mu=2, n_az=4)
+    s = pk.SweepSolver(prob)
+    s.zero_block_for_test(5, 3)
+    with pytest.raises(pk.SolverError, match=r"element 5.*ordinate 3"):
+        s.sweep(-1, np.zeros(s.num_dofs), np.zeros((s.num_ordinates, s.num_dofs)))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_single_hex_element_all_orders(p):
+    """Edge case: one twisted hexahedron (every face on the boundary), orders 1-4."""
+    pts, nodes, bf = pb.generate_uniform_3d(1, 1, 1, p)
+    pts = pb.twist_3d(pts, 0.7)
+    w, d = pb.product_quadrature(3, 2, 4)
+    prob = pb.Problem(3, p, p, pts, nodes, np.ones(1, np.int32), bf, w, d, {1: (2.0, 1.0)}, 0, (1.0,))
+    gpu = pk.SweepSolver(prob)
+    orc = O.OracleSolver(prob)
+    phi, psi_old = _inputs(prob, 23)
+    assert rel_l2(gpu.sweep(-1, phi, psi_old), orc.sweep_all(phi, psi_old)) <= SWEEP_TOL
