@@ -1307,6 +1307,10 @@ struct hsw_handle {
         std::vector<int> offsets;   // num_levels + 1
     };
     std::map<std::pair<int, int>, RangeList> ranges;
+    // host-pointer all-ordinate sweep: copy streams and per-block events
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_sw;
+    cudaEvent_t ev_cp[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -1344,6 +1348,12 @@ void free_handle(hsw_handle* h) {
         if (b) cudaFree(b);
     for (auto& kv : h->ranges)
         if (kv.second.d_pairs) cudaFree(kv.second.d_pairs);
+    for (auto e : h->ev_in) cudaEventDestroy(e);
+    for (auto e : h->ev_sw) cudaEventDestroy(e);
+    for (auto e : h->ev_cp)
+        if (e) cudaEventDestroy(e);
+    if (h->copy_in) cudaStreamDestroy(h->copy_in);
+    if (h->copy_out) cudaStreamDestroy(h->copy_out);
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1421,6 +1431,32 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
     }
     if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
     h->last_launches = launches;
+}
+
+// Ordinate blocks of the pipelined host-pointer sweep: 4 when psi is large
+// enough for PCIe time to matter (HSW_E2E_BLOCKS overrides; 1 disables).
+int e2e_blocks(const hsw_handle* h) {
+    static const int env = [] {
+        const char* v = std::getenv("HSW_E2E_BLOCKS");
+        return v ? std::atoi(v) : 0;
+    }();
+    int b = env > 0 ? env : ((double)h->N * h->S.nd * sizeof(double) >= 64e6 ? 4 : 1);
+    return std::max(1, std::min(b, h->S.nd));
+}
+
+void ensure_copy_streams(hsw_handle* h, int nblk) {
+    if (!h->copy_in) {
+        CUDA_OK(cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+        for (auto& e : h->ev_cp) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    while ((int)h->ev_in.size() < nblk) {
+        cudaEvent_t a, b;
+        CUDA_OK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        h->ev_in.push_back(a);
+        h->ev_sw.push_back(b);
+    }
 }
 
 // Worklist of the ordinate block [d0, d1): the all-ordinate list filtered,
@@ -1723,10 +1759,39 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
         const size_t N = h->N;
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         if (d == -1) {
-            CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi_old, N * h->S.nd * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-            dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
-            run_all_levels(h, h->d_psiA, h->d_psiB, false);
-            CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB, N * h->S.nd * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            const int nd = h->S.nd;
+            const int nblk = e2e_blocks(h);
+            if (nblk <= 1) {
+                CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi_old, N * nd * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+                dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+                run_all_levels(h, h->d_psiA, h->d_psiB, false);
+                CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB, N * nd * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            } else {
+                // Pipelined over ordinate blocks: a block's sweep needs only its own
+                // psi_old (lagged couplings stay within an ordinate), so the H2D of
+                // block b+1 and the D2H of block b-1 overlap the sweep of block b.
+                ensure_copy_streams(h, nblk);
+                CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
+                CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
+                dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+                for (int b = 0; b < nblk; ++b) {
+                    const int d0 = (int)((int64_t)b * nd / nblk), d1 = (int)((int64_t)(b + 1) * nd / nblk);
+                    const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
+                    CUDA_OK(cudaMemcpyAsync(h->d_psiA + off, psi_old + off, cnt, cudaMemcpyHostToDevice, h->copy_in));
+                    CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
+                }
+                for (int b = 0; b < nblk; ++b) {
+                    const int d0 = (int)((int64_t)b * nd / nblk), d1 = (int)((int64_t)(b + 1) * nd / nblk);
+                    const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
+                    CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
+                    run_range_levels(h, range_list(h, d0, d1), h->d_psiA, h->d_psiB);
+                    CUDA_OK(cudaEventRecord(h->ev_sw[b], h->stream));
+                    CUDA_OK(cudaStreamWaitEvent(h->copy_out, h->ev_sw[b], 0));
+                    CUDA_OK(cudaMemcpyAsync(psi_new + off, h->d_psiB + off, cnt, cudaMemcpyDeviceToHost, h->copy_out));
+                }
+                CUDA_OK(cudaEventRecord(h->ev_cp[1], h->copy_out));
+                CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_cp[1], 0));
+            }
         } else {
             double* slotA = h->d_psiA + (size_t)d * N;
             double* slotB = h->d_psiB + (size_t)d * N;
