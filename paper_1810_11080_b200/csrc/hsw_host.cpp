@@ -1016,19 +1016,37 @@ struct Setup {
     }
 
     // assembly.hpp:58-93 + 143-163 + 278-300: per element M, G_k, volume source
-    void element_tensors() {
-        // basis tables at the volume points (element independent)
-        std::vector<double> U((size_t)nq * nb), DU((size_t)nq * nb * dim);
-        std::vector<double> GV((size_t)nq * mesh.npe), GG((size_t)nq * mesh.npe * dim);
+    // basis / geometry tables at the volume points (element independent)
+    std::vector<double> volU, volDU, volGV, volGG;
+    void volume_tables() {
+        volU.assign((size_t)nq * nb, 0.0);
+        volDU.assign((size_t)nq * nb * dim, 0.0);
+        volGV.assign((size_t)nq * mesh.npe, 0.0);
+        volGG.assign((size_t)nq * mesh.npe * dim, 0.0);
         for (int q = 0; q < nq; ++q) {
-            basis.values(vq_pts[q].data(), &U[(size_t)q * nb]);
-            basis.gradients(vq_pts[q].data(), &DU[(size_t)q * nb * dim]);
-            mesh.geom.values(vq_pts[q].data(), &GV[(size_t)q * mesh.npe]);
-            mesh.geom.gradients(vq_pts[q].data(), &GG[(size_t)q * mesh.npe * dim]);
+            basis.values(vq_pts[q].data(), &volU[(size_t)q * nb]);
+            basis.gradients(vq_pts[q].data(), &volDU[(size_t)q * nb * dim]);
+            mesh.geom.values(vq_pts[q].data(), &volGV[(size_t)q * mesh.npe]);
+            mesh.geom.gradients(vq_pts[q].data(), &volGG[(size_t)q * mesh.npe * dim]);
         }
-        T.assign((size_t)nel * nb * nb * 4, 0.0);
+    }
+
+    // host_T = false: only the materials here; T and the source moments are
+    // computed on the device (hsw_setup.cu) at hsw_create
+    void element_tensors(bool host_T = true) {
+        volume_tables();
         sig_t.resize(nel);
         sig_s.resize(nel);
+        for (int e = 0; e < nel; ++e) {
+            sig_t[e] = xs_t(mesh.region[e]);
+            sig_s[e] = xs_s(mesh.region[e]);
+        }
+        if (!host_T) return;
+        const std::vector<double>& U = volU;
+        const std::vector<double>& DU = volDU;
+        const std::vector<double>& GV = volGV;
+        const std::vector<double>& GG = volGG;
+        T.assign((size_t)nel * nb * nb * 4, 0.0);
         qvol.assign((size_t)nel * nb, 0.0);
         if (weighting == HSW_WEIGHT_SIGINVFACE) mass_t_cache.assign((size_t)nel * nb * nb, 0.0);
         parallel_for(nel, [&](int64_t e64) {
@@ -1534,12 +1552,30 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
     hsw_handle* h = new hsw_handle();
     const int rc = guarded([&] {
         Setup& S = h->S;
+        // HSW_SETUP_TIMING=1 prints the host setup phases (stderr)
+        static const bool timing = std::getenv("HSW_SETUP_TIMING") != nullptr;
+        auto tick = std::chrono::steady_clock::now();
+        auto phase = [&](const char* name) {
+            if (!timing) return;
+            const auto now = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "hsw setup %-16s %8.3f s\n", name, std::chrono::duration<double>(now - tick).count());
+            tick = now;
+        };
         S.ingest(desc);
+        phase("ingest");
         S.build_mesh(desc->num_points, desc->validate_geometry != 0);
-        S.element_tensors();
+        phase("build_mesh");
+        // element tensors on the device unless host-only, or the siginvface weights
+        // need the host's exact M_t arithmetic (sweepgraph.hpp:65-72)
+        const bool host_T = desc->device < 0 || S.weighting == HSW_WEIGHT_SIGINVFACE;
+        S.element_tensors(host_T);
+        phase("element_tensors");
         S.face_tables();
+        phase("face_tables");
         S.ordinates();
+        phase("ordinates");
         S.worklists();
+        phase("worklists");
         // device (device < 0: host-only plan, used by the CPU tests of the host logic)
         if (desc->device < 0) return HSW_OK;
         int ndev = 0;
@@ -1579,10 +1615,41 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             h->d_tab_nmask = dev_upload(nmask);
             h->d_tab_line = dev_upload(line);
         }
-        h->d_T = dev_upload(S.T);
+        if (!S.T.empty()) {
+            h->d_T = dev_upload(S.T);
+            h->d_qvol = dev_upload(S.qvol);
+        } else {   // element tensors + source moments computed on the device (hsw_setup.cu)
+            const size_t nb = (size_t)S.nb, nel = (size_t)S.nel;
+            CUDA_OK(cudaMalloc(&h->d_T, nel * nb * nb * 4 * sizeof(double)));
+            CUDA_OK(cudaMalloc(&h->d_qvol, nel * nb * sizeof(double)));
+            double* d_pts = dev_upload(S.mesh.pts);
+            int* d_en = dev_upload(S.mesh.enodes);
+            double* d_U = dev_upload(S.volU);
+            double* d_DU = dev_upload(S.volDU);
+            double* d_GG = dev_upload(S.volGG);
+            double* d_GV = dev_upload(S.volGV);
+            double* d_w = dev_upload(S.vq_w);
+            unsigned long long* d_bad = nullptr;
+            CUDA_OK(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+            CUDA_OK(cudaMemset(d_bad, 0xff, sizeof(unsigned long long)));
+            SourceParams sp{};
+            for (int i = 0; i < 8; ++i) sp.v[i] = S.source_params[i];
+            dev_element_tensors(S.dim, S.nel, S.nb, S.mesh.npe, S.nq, d_pts, d_en, d_U, d_DU, d_GG, d_GV, d_w,
+                                S.source_kind, sp, h->d_T, h->d_qvol, d_bad, h->stream);
+            unsigned long long bad = 0;
+            S.qvol.resize(nel * nb);
+            CUDA_OK(cudaMemcpyAsync(S.qvol.data(), h->d_qvol, nel * nb * sizeof(double), cudaMemcpyDeviceToHost,
+                                    h->stream));
+            CUDA_OK(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
+            CUDA_OK(cudaStreamSynchronize(h->stream));
+            for (void* b : {(void*)d_pts, (void*)d_en, (void*)d_U, (void*)d_DU, (void*)d_GG, (void*)d_GV, (void*)d_w,
+                            (void*)d_bad})
+                cudaFree(b);
+            if (bad != ~0ull)
+                throw hsw::Error(HSW_ERR_ASSEMBLY, "assembly: singular Jacobian in element " + std::to_string(bad));
+        }
         h->d_sig_t = dev_upload(S.sig_t);
         h->d_sig_s = dev_upload(S.sig_s);
-        h->d_qvol = dev_upload(S.qvol);
         h->d_fgeom = dev_upload(S.fgeom);
         h->d_fnbr = dev_upload(S.fnbr);
         h->d_inflags = dev_upload(S.inflags);
@@ -1950,11 +2017,18 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
             inflow_tot += w * inf_d;
         }
         // absorption: (M_t - M_s) phi summed, with M_t - M_s = (sigma_t - sigma_s) M
-        for (int e = 0; e < S.nel; ++e) {
-            const double sa = S.sig_t[e] - S.sig_s[e];
-            const double* Te = &S.T[(size_t)e * nb * nb * 4];
-            for (int m = 0; m < nb; ++m)
-                for (int n = 0; n < nb; ++n) absorption += sa * Te[((size_t)n * nb + m) * 4] * phi[(size_t)e * nb + n];
+        if (!S.T.empty()) {
+            for (int e = 0; e < S.nel; ++e) {
+                const double sa = S.sig_t[e] - S.sig_s[e];
+                const double* Te = &S.T[(size_t)e * nb * nb * 4];
+                for (int m = 0; m < nb; ++m)
+                    for (int n = 0; n < nb; ++n)
+                        absorption += sa * Te[((size_t)n * nb + m) * 4] * phi[(size_t)e * nb + n];
+            }
+        } else {   // the element tensors live on the device only
+            need_device(h);
+            CUDA_OK(cudaMemcpyAsync(h->d_vec, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            absorption = dev_absorption(S.nel, nb, h->d_T, h->d_sig_t, h->d_sig_s, h->d_vec, h->d_scratch, h->stream);
         }
         out5[0] = sv;
         out5[1] = inflow_tot;

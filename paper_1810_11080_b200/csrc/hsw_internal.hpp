@@ -47,6 +47,10 @@ struct DevProblem {
 };
 
 // Host-computed tables that are uploaded to constant memory.
+struct SourceParams {
+    double v[8];
+};
+
 struct ConstTables {
     int fnode[kMaxFaces][kMaxFaceNodes];                 // local element node of face node a
     double trace[kMaxFacePoints][kMaxFaceNodes];         // phi_a(point q) on the reference face
@@ -89,6 +93,13 @@ void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_ol
                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
 void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                           unsigned long long* err_key, int64_t zero_pair, void* stream);
+// device-side setup (hsw_setup.cu): element tensors + volume source moments, absorption
+void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double* pts, const int* enodes,
+                         const double* U, const double* DU, const double* GG, const double* GV, const double* wq,
+                         int source_kind, const SourceParams& sp, double* T, double* qvol,
+                         unsigned long long* bad_elem, void* stream);
+double dev_absorption(int nel, int nb, const double* T, const double* sig_t, const double* sig_s, const double* phi,
+                      double* scratch, void* stream);
 // direction-sharded source iteration (hsw_kernels.cu)
 void dev_phi_partial(const DevProblem& P, const double* psi_new, int d0, int d1, const double* prefix, double* out,
                      void* stream);

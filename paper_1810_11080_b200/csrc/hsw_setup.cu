@@ -1,0 +1,205 @@
+// Device-side setup: per-element tensors T = [M, G_x, G_y, G_z] and volume
+// source moments, computed where they are used instead of on the host and
+// uploaded (C4: 4.3 GB of T, ~8 s of host time on 8 cores -> milliseconds).
+//
+// Replaces the direction-independent half of assemble_volume / assemble_source
+// (assembly.hpp:143-163, 292-300) hoisted out of the ordinate loop
+// (SURVEY §8a A4-A7):
+//   M[m][n]   =  sum_q w_q det_q u_m(x_q) u_n(x_q)
+//   G_k[m][n] = -sum_q w_q det_q (d_k u_m)(x_q) u_n(x_q),  grad = J^{-T} grad_ref
+//   qvol[m]   =  sum_q w_q det_q q(x_q) u_m(x_q)
+// Layout: T[e][n][m][k] (column-major per element, k = 0..3) as hsw_host.cpp's
+// host path; tolerance-level (not bit-level) agreement with it: T feeds only
+// the FP64 solves, never an integer decision.
+#include "hsw_internal.hpp"
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+namespace hsw {
+
+#define SCHECK(x)                                                                              \
+    do {                                                                                       \
+        cudaError_t _e = (x);                                                                  \
+        if (_e != cudaSuccess)                                                                 \
+            throw Error(-8, std::string("CUDA: ") + cudaGetErrorString(_e) + " at " #x);       \
+    } while (0)
+
+namespace {
+
+constexpr int kSetupThreads = 256;
+constexpr int kMaxQ = 216;   // (p + 2)^3 volume points, p <= 4
+
+template <int DIM>
+__global__ void __launch_bounds__(kSetupThreads)
+element_tensor_kernel(int nel, int nb, int npe, int nq, const double* __restrict__ pts, const int* __restrict__ enodes,
+                      const double* __restrict__ U, const double* __restrict__ DU, const double* __restrict__ GG,
+                      const double* __restrict__ GV, const double* __restrict__ wq, int source_kind,
+                      SourceParams sp, double* __restrict__ T, double* __restrict__ qvol,
+                      unsigned long long* __restrict__ bad_elem) {
+    __shared__ double sK[kMaxQ][DIM * DIM];   // J^{-1}
+    __shared__ double sW[kMaxQ];              // w_q det_q
+    __shared__ double sS[kMaxQ];              // w_q det_q q(x_q)
+    const int e = blockIdx.x;
+    const int* en = enodes + (size_t)e * npe;
+    // 1. geometry at the volume points (mesh.hpp:157-170)
+    for (int q = threadIdx.x; q < nq; q += kSetupThreads) {
+        double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, x[3] = {0, 0, 0};
+        const double* g = GG + (size_t)q * npe * DIM;
+        const double* v = GV + (size_t)q * npe;
+        for (int m = 0; m < npe; ++m) {
+            const double* X = pts + (size_t)en[m] * DIM;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+#pragma unroll
+                for (int b = 0; b < DIM; ++b) J[a * 3 + b] += X[a] * g[m * DIM + b];
+                x[a] += v[m] * X[a];
+            }
+        }
+        double det, K[9];
+        if (DIM == 2) {
+            det = J[0] * J[4] - J[3] * J[1];
+            const double id = 1.0 / det;
+            K[0] = J[4] * id; K[3] = -J[3] * id; K[1] = -J[1] * id; K[4] = J[0] * id;
+        } else {
+            const double c00 = J[4] * J[8] - J[5] * J[7];
+            const double c01 = J[5] * J[6] - J[3] * J[8];
+            const double c02 = J[3] * J[7] - J[4] * J[6];
+            det = J[0] * c00 + J[1] * c01 + J[2] * c02;
+            const double id = 1.0 / det;
+            K[0] = c00 * id; K[1] = (J[2] * J[7] - J[1] * J[8]) * id; K[2] = (J[1] * J[5] - J[2] * J[4]) * id;
+            K[3] = c01 * id; K[4] = (J[0] * J[8] - J[2] * J[6]) * id; K[5] = (J[2] * J[3] - J[0] * J[5]) * id;
+            K[6] = c02 * id; K[7] = (J[1] * J[6] - J[0] * J[7]) * id; K[8] = (J[0] * J[4] - J[1] * J[3]) * id;
+        }
+        if (!(det > 0.0) || !isfinite(det)) atomicMin(bad_elem, (unsigned long long)e);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) sK[q][a * DIM + b] = K[a * 3 + b];
+        const double wd = wq[q] * det;
+        sW[q] = wd;
+        double src = sp.v[0];
+        if (source_kind != 0) {   // disc / ball (assembly.hpp:298 at the quadrature point)
+            double d2 = 0.0;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) d2 += (x[a] - sp.v[a]) * (x[a] - sp.v[a]);
+            src = d2 < sp.v[3] * sp.v[3] ? sp.v[4] : sp.v[5];
+        }
+        sS[q] = wd * src;
+    }
+    __syncthreads();
+    // 2. source moments
+    for (int m = threadIdx.x; m < nb; m += kSetupThreads) {
+        double s = 0.0;
+        for (int q = 0; q < nq; ++q) s += sS[q] * U[(size_t)q * nb + m];
+        qvol[(size_t)e * nb + m] = s;
+    }
+    // 3. T in 4 x 4 (m, n) blocks per thread, all DIM + 1 components
+    const int nbb = (nb + 3) / 4;
+    double* Te = T + (size_t)e * nb * nb * 4;
+    for (int blk = threadIdx.x; blk < nbb * nbb; blk += kSetupThreads) {
+        const int m0 = 4 * (blk / nbb), n0 = 4 * (blk % nbb);
+        double acc[4][4][DIM + 1];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k = 0; k <= DIM; ++k) acc[i][j][k] = 0.0;
+        for (int q = 0; q < nq; ++q) {
+            const double wd = sW[q];
+            double wm[4][DIM + 1], un[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = min(m0 + i, nb - 1);
+                wm[i][0] = U[(size_t)q * nb + m] * wd;
+                const double* du = DU + ((size_t)q * nb + m) * DIM;
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int j = 0; j < DIM; ++j) v += sK[q][j * DIM + k] * du[j];
+                    wm[i][k + 1] = v * wd;
+                }
+                un[i] = U[(size_t)q * nb + min(n0 + i, nb - 1)];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int k = 0; k <= DIM; ++k) acc[i][j][k] += wm[i][k] * un[j];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int m = m0 + i, n = n0 + j;
+                if (m < nb && n < nb) {
+                    double* o = Te + ((size_t)n * nb + m) * 4;
+                    o[0] = acc[i][j][0];
+#pragma unroll
+                    for (int k = 1; k <= DIM; ++k) o[k] = -acc[i][j][k];
+                    if (DIM == 2) o[3] = 0.0;
+                }
+            }
+    }
+}
+
+// absorption = sum_e (sigma_t - sigma_s) 1^T M_e phi_e (balance_report, solver.hpp:220-245)
+__global__ void __launch_bounds__(256)
+absorption_kernel(int nel, int nb, const double* __restrict__ T, const double* __restrict__ sig_t,
+                  const double* __restrict__ sig_s, const double* __restrict__ phi, double* __restrict__ part) {
+    double s = 0.0;
+    const int64_t total = (int64_t)nel * nb;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(i / nb), n = (int)(i % nb);
+        const double* col = T + ((size_t)e * nb * nb + (size_t)n * nb) * 4;   // column n: M[m][n], m = 0..nb-1
+        double cs = 0.0;
+        for (int m = 0; m < nb; ++m) cs += col[(size_t)m * 4];
+        s += (sig_t[e] - sig_s[e]) * cs * phi[i];
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+}  // namespace
+
+void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double* pts, const int* enodes,
+                         const double* U, const double* DU, const double* GG, const double* GV, const double* wq,
+                         int source_kind, const SourceParams& sp, double* T, double* qvol,
+                         unsigned long long* bad_elem, void* stream) {
+    if (nq > kMaxQ) throw Error(-1, "dev_element_tensors: too many volume points");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dim == 2)
+        element_tensor_kernel<2><<<nel, kSetupThreads, 0, st>>>(nel, nb, npe, nq, pts, enodes, U, DU, GG, GV, wq,
+                                                                source_kind, sp, T, qvol, bad_elem);
+    else
+        element_tensor_kernel<3><<<nel, kSetupThreads, 0, st>>>(nel, nb, npe, nq, pts, enodes, U, DU, GG, GV, wq,
+                                                                source_kind, sp, T, qvol, bad_elem);
+    SCHECK(cudaGetLastError());
+}
+
+double dev_absorption(int nel, int nb, const double* T, const double* sig_t, const double* sig_s, const double* phi,
+                      double* scratch, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nblk = 1024;
+    absorption_kernel<<<nblk, 256, 0, st>>>(nel, nb, T, sig_t, sig_s, phi, scratch);
+    SCHECK(cudaGetLastError());
+    std::vector<double> h(nblk);
+    SCHECK(cudaMemcpyAsync(h.data(), scratch, nblk * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SCHECK(cudaStreamSynchronize(st));
+    double s = 0.0;
+    for (double v : h) s += v;
+    return s;
+}
+
+}  // namespace hsw
