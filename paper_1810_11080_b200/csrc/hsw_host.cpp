@@ -831,6 +831,9 @@ struct Setup {
     // face trace tables (bit-exact with the reference element-wise arithmetic)
     std::vector<double> trace;              // nqf * nfn: phi_a at own param point q
     std::vector<std::vector<double>> traceR;  // per orientation code: nqf * nfn at mapped point
+    // max|LR|, max|RL| per (ordinate, interior face) computed on the device
+    // (hsw_setup.cu, bit-identical to the host loop below); empty: host computes
+    std::vector<double> dev_cmax;
     // per ordinate
     std::vector<std::vector<Coupling>> couplings;
     std::vector<std::vector<double>> weights;
@@ -1174,6 +1177,21 @@ struct Setup {
                 std::fill(RL.begin(), RL.end(), 0.0);
                 double length = 0.0;
                 const double* uR0 = traceR[F.orient].data();
+                if (!dev_cmax.empty()) {   // magnitudes from the device; length here
+                    double length = 0.0;
+                    for (int q = 0; q < nqf; ++q) length += fq_w[q] * sjv[q];
+                    const double eps = 1e-12 * length;
+                    const double mlr = dev_cmax[((size_t)d * nfi + fi) * 2], mrl = dev_cmax[((size_t)d * nfi + fi) * 2 + 1];
+                    if (mlr > eps) {
+                        cpl.push_back({fi, F.el, F.er, F.fl, F.fr});
+                        wts.push_back(weight_of(mlr, F.el, F.fl, LR, false));
+                    }
+                    if (mrl > eps) {
+                        cpl.push_back({fi, F.er, F.el, F.fr, F.fl});
+                        wts.push_back(weight_of(mrl, F.er, F.fr, RL, false));
+                    }
+                    continue;
+                }
                 for (int q = 0; q < nqf; ++q) {
                     double on = 0.0;
                     for (int k = 0; k < dim; ++k) on += om[k] * geo[q * 4 + k];
@@ -1546,6 +1564,57 @@ int hsw_last_error(char* buf, size_t len) {
     return (int)g_last_error.size();
 }
 
+namespace {
+void device_init(hsw_handle* h, int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw hsw::Error(HSW_ERR_CUDA, "hsw_create: no CUDA device available (the B200 sweep has no CPU fallback)");
+    h->device = device;
+    CUDA_OK(cudaSetDevice(h->device));
+    CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&h->ev0));
+    CUDA_OK(cudaEventCreate(&h->ev1));
+}
+
+// max|LR|, max|RL| of every (ordinate, interior face) on the device, in blocks
+// of ordinates, into S.dev_cmax for Setup::ordinates
+void device_coupling_max(hsw_handle* h) {
+    Setup& S = h->S;
+    const int nfi = (int)S.mesh.ifaces.size();
+    S.dev_cmax.assign((size_t)S.nd * nfi * 2, 0.0);
+    if (nfi == 0) return;
+    std::vector<int> iface((size_t)nfi * 5);
+    for (int i = 0; i < nfi; ++i) {
+        const IFace& F = S.mesh.ifaces[i];
+        int* r = &iface[(size_t)i * 5];
+        r[0] = F.el; r[1] = F.er; r[2] = F.fl; r[3] = F.fr; r[4] = F.orient;
+    }
+    std::vector<double> trR;
+    for (const auto& t : S.traceR) trR.insert(trR.end(), t.begin(), t.end());
+    int* d_if = dev_upload(iface);
+    double* d_geo = dev_upload(S.fgeom);
+    double* d_sj = dev_upload(S.fsj);
+    double* d_w = dev_upload(S.fq_w);
+    double* d_tr = dev_upload(S.trace);
+    double* d_trR = dev_upload(trR);
+    double* d_od = dev_upload(S.odir);
+    const int chunk = std::max(1, std::min(S.nd, (int)(std::max<size_t>(1, (size_t)(256u << 20) / ((size_t)nfi * 16)))));
+    double* d_out = nullptr;
+    CUDA_OK(cudaMalloc(&d_out, (size_t)chunk * nfi * 2 * sizeof(double)));
+    for (int d0 = 0; d0 < S.nd; d0 += chunk) {
+        const int d1 = std::min(S.nd, d0 + chunk);
+        dev_coupling_max(S.dim, nfi, S.nf, S.nqf, S.nfn, d_if, d_geo, d_sj, d_w, d_tr, d_trR, d_od, d0, d1, d_out,
+                         h->stream);
+        CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)d0 * nfi * 2], d_out, (size_t)(d1 - d0) * nfi * 2 * sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+    }
+    CUDA_OK(cudaStreamSynchronize(h->stream));
+    for (void* b : {(void*)d_if, (void*)d_geo, (void*)d_sj, (void*)d_w, (void*)d_tr, (void*)d_trR, (void*)d_od,
+                    (void*)d_out})
+        cudaFree(b);
+}
+}  // namespace
+
 int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
     if (!out) return fail(HSW_ERR_INVALID, "hsw_create: null output handle");
     *out = nullptr;
@@ -1572,20 +1641,21 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         phase("element_tensors");
         S.face_tables();
         phase("face_tables");
+        if (desc->device >= 0) {
+            device_init(h, desc->device);
+            if (S.weighting != HSW_WEIGHT_SIGINVFACE) {   // siginvface needs the blocks on the host
+                device_coupling_max(h);
+                phase("couplings(dev)");
+            }
+        }
         S.ordinates();
         phase("ordinates");
         S.worklists();
         phase("worklists");
         // device (device < 0: host-only plan, used by the CPU tests of the host logic)
         if (desc->device < 0) return HSW_OK;
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-            throw hsw::Error(HSW_ERR_CUDA, "hsw_create: no CUDA device available (the B200 sweep has no CPU fallback)");
-        h->device = desc->device;
-        CUDA_OK(cudaSetDevice(h->device));
-        CUDA_OK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-        CUDA_OK(cudaEventCreate(&h->ev0));
-        CUDA_OK(cudaEventCreate(&h->ev1));
+        S.dev_cmax.clear();
+        S.dev_cmax.shrink_to_fit();
         ConstTables ct{};
         for (int f = 0; f < S.nf; ++f)
             for (int a = 0; a < S.nfn; ++a) ct.fnode[f][a] = S.fnodes[f][a];

@@ -100,6 +100,9 @@ void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double
                          unsigned long long* bad_elem, void* stream);
 double dev_absorption(int nel, int nb, const double* T, const double* sig_t, const double* sig_s, const double* phi,
                       double* scratch, void* stream);
+void dev_coupling_max(int dim, int nfi, int nf, int nqf, int nfn, const int* iface, const double* fgeom,
+                      const double* fsj, const double* fqw, const double* trace, const double* traceR,
+                      const double* odir, int d0, int d1, double* out, void* stream);
 // direction-sharded source iteration (hsw_kernels.cu)
 void dev_phi_partial(const DevProblem& P, const double* psi_new, int d0, int d1, const double* prefix, double* out,
                      void* stream);

@@ -202,4 +202,84 @@ double dev_absorption(int nel, int nb, const double* T, const double* sig_t, con
     return s;
 }
 
+
+// ---- per-(ordinate, interior face) coupling magnitudes
+// max|LR| and max|RL| of the two coupling blocks of every interior face for a
+// block of ordinates: the edge-existence test (> 1e-12 * length) and the `face`
+// edge weight of sweepgraph.hpp:60-64.  Bit-identical to the host
+// (hsw_host.cpp Setup::ordinates, itself the restatement of
+// assembly.hpp:197-241): same inputs, ascending quadrature order, every
+// product / sum rounded separately (__dmul_rn / __dadd_rn: no FMA contraction).
+namespace {
+constexpr int kCplThreads = 256;
+
+__global__ void __launch_bounds__(kCplThreads)
+coupling_max_kernel(int dim, int nfi, int nf, int nqf, int nfn, const int* __restrict__ iface /*[nfi][5]*/,
+                    const double* __restrict__ fgeom, const double* __restrict__ fsj, const double* __restrict__ fqw,
+                    const double* __restrict__ trace /*[nqf][nfn]*/, const double* __restrict__ traceR /*[code][nqf][nfn]*/,
+                    const double* __restrict__ odir /*[nd][3]*/, int d0, int d1, double* __restrict__ out /*[d][nfi][2]*/) {
+    __shared__ double s_geo[64 * 4], s_sj[64], s_wm[64], s_wp[64];
+    __shared__ double s_red[2][kCplThreads / 32];
+    const int fi = blockIdx.x;
+    const int el = iface[fi * 5 + 0], fl = iface[fi * 5 + 2], orient = iface[fi * 5 + 4];
+    for (int i = threadIdx.x; i < nqf * 4; i += kCplThreads) s_geo[i] = fgeom[((size_t)el * nf + fl) * nqf * 4 + i];
+    for (int i = threadIdx.x; i < nqf; i += kCplThreads) s_sj[i] = fsj[((size_t)el * nf + fl) * nqf + i];
+    const double* uR = traceR + (size_t)orient * nqf * nfn;
+    for (int d = d0; d < d1; ++d) {
+        __syncthreads();   // s_wm / s_wp reuse
+        for (int q = threadIdx.x; q < nqf; q += kCplThreads) {
+            double on = 0.0;
+            for (int k = 0; k < dim; ++k) on = __dadd_rn(on, __dmul_rn(odir[d * 3 + k], s_geo[q * 4 + k]));
+            s_wp[q] = __dmul_rn(0.5, __dadd_rn(on, fabs(on)));
+            s_wm[q] = __dmul_rn(0.5, __dadd_rn(fabs(on), -on));
+        }
+        __syncthreads();
+        double mlr = 0.0, mrl = 0.0;
+        for (int mn = threadIdx.x; mn < nfn * nfn; mn += kCplThreads) {
+            const int m = mn / nfn, n = mn - m * nfn;
+            double lr = 0.0, rl = 0.0;
+            for (int q = 0; q < nqf; ++q) {
+                const double w = fqw[q], sj = s_sj[q];
+                const double ul_m = trace[q * nfn + m], ur_n = uR[q * nfn + n];
+                const double ur_m = uR[q * nfn + m], ul_n = trace[q * nfn + n];
+                // row[n] += w * (c * ur[n] * sj), c = w- * ul[m]   (and the mirrored RL term)
+                lr = __dadd_rn(lr, __dmul_rn(w, __dmul_rn(__dmul_rn(__dmul_rn(s_wm[q], ul_m), ur_n), sj)));
+                rl = __dadd_rn(rl, __dmul_rn(w, __dmul_rn(__dmul_rn(__dmul_rn(s_wp[q], ur_m), ul_n), sj)));
+            }
+            mlr = fmax(mlr, fabs(lr));
+            mrl = fmax(mrl, fabs(rl));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            mlr = fmax(mlr, __shfl_xor_sync(0xffffffffu, mlr, off));
+            mrl = fmax(mrl, __shfl_xor_sync(0xffffffffu, mrl, off));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_red[0][threadIdx.x >> 5] = mlr;
+            s_red[1][threadIdx.x >> 5] = mrl;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < kCplThreads / 32; ++w) {
+                a = fmax(a, s_red[0][w]);
+                b = fmax(b, s_red[1][w]);
+            }
+            out[((size_t)(d - d0) * nfi + fi) * 2 + 0] = a;
+            out[((size_t)(d - d0) * nfi + fi) * 2 + 1] = b;
+        }
+    }
+}
+}  // namespace
+
+void dev_coupling_max(int dim, int nfi, int nf, int nqf, int nfn, const int* iface, const double* fgeom,
+                      const double* fsj, const double* fqw, const double* trace, const double* traceR,
+                      const double* odir, int d0, int d1, double* out, void* stream) {
+    if (nqf > 64) throw Error(-1, "dev_coupling_max: too many face points");
+    if (nfi == 0 || d1 <= d0) return;
+    coupling_max_kernel<<<nfi, kCplThreads, 0, (cudaStream_t)stream>>>(dim, nfi, nf, nqf, nfn, iface, fgeom, fsj, fqw,
+                                                                       trace, traceR, odir, d0, d1, out);
+    SCHECK(cudaGetLastError());
+}
+
 }  // namespace hsw

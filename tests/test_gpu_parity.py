@@ -169,3 +169,21 @@ def test_single_hex_element_all_orders(p):
     orc = O.OracleSolver(prob)
     phi, psi_old = _inputs(prob, 23)
     assert rel_l2(gpu.sweep(-1, phi, psi_old), orc.sweep_all(phi, psi_old)) <= SWEEP_TOL
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c2", dict(cells=24, n_mu=2, n_az=8)),
+                                     ("c3", dict(cells=6, n_mu=4, n_az=8)), ("c4", dict(cells=6, n_mu=2, n_az=8)),
+                                     ("c5", dict(cells=4, n_mu=2, n_az=8))])
+def test_device_coupling_magnitudes_give_the_host_plan(name, kw):
+    """the per-(ordinate, face) coupling magnitudes computed on
+    the device drive edge existence and weights; the resulting graphs, cut sets,
+    orders and levels equal the host-only plan bit for bit."""
+    prob = pb.config(name, **kw)
+    dev = pk.SweepSolver(prob)
+    host = pk.SweepSolver(prob, device=-1)
+    assert dev.total_lagged_edges() == host.total_lagged_edges()
+    for d in range(prob.num_ordinates):
+        a, b = dev.ordering(d), host.ordering(d)
+        assert (a.order == b.order).all() and (a.position == b.position).all()
+        assert (a.lagged_edges == b.lagged_edges).all() and a.lagged_weight == b.lagged_weight
+        assert (a.level == b.level).all()
