@@ -38,6 +38,7 @@
 #include <numeric>
 #include <queue>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 namespace hsw {
@@ -1343,6 +1344,24 @@ struct hsw_handle {
         std::vector<int> offsets;   // num_levels + 1
     };
     std::map<std::pair<int, int>, RangeList> ranges;
+    // captured all-ordinate level sequences (CUDA graphs)
+    struct GraphKey {
+        const double* psi_old;
+        const double* psi_new;
+        int flags;
+        int64_t zero_pair;
+        int kernel;
+        bool operator<(const GraphKey& o) const {
+            return std::tie(psi_old, psi_new, flags, zero_pair, kernel) <
+                   std::tie(o.psi_old, o.psi_new, o.flags, o.zero_pair, o.kernel);
+        }
+    };
+    struct GraphEntry {
+        cudaGraphExec_t exec;
+        int64_t launches;
+    };
+    std::map<GraphKey, GraphEntry> graphs;
+    bool levels_configured = false;
     // host-pointer all-ordinate sweep: copy streams and per-block events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_sw;
@@ -1384,6 +1403,7 @@ void free_handle(hsw_handle* h) {
         if (b) cudaFree(b);
     for (auto& kv : h->ranges)
         if (kv.second.d_pairs) cudaFree(kv.second.d_pairs);
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto e : h->ev_in) cudaEventDestroy(e);
     for (auto e : h->ev_sw) cudaEventDestroy(e);
     for (auto e : h->ev_cp)
@@ -1455,9 +1475,8 @@ void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const i
 }
 
 // All-ordinate sweep psi_old -> psi_new using the current h->d_src.
-void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
+int64_t launch_all_levels(hsw_handle* h, const double* psi_old, double* psi_new) {
     const auto& off = h->S.level_offsets;
-    if (time_it) CUDA_OK(cudaEventRecord(h->ev0, h->stream));
     int64_t launches = 0;
     for (int l = 0; l < h->S.num_levels; ++l) {
         const int n = off[l + 1] - off[l];
@@ -1465,8 +1484,47 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
         sweep_launch(h, psi_old, psi_new, h->d_pairs_all + off[l], n);
         ++launches;
     }
+    return launches;
+}
+
+bool graphs_enabled() {
+    static const bool v = [] { const char* e = std::getenv("HSW_GRAPHS"); return !(e && e[0] == '0'); }();
+    return v;
+}
+
+// The all-ordinate sweep is one launch per level (C2: 449 levels of ~24 us):
+// after a first direct run (which configures every kernel), the level sequence
+// is captured once per (psi_old, psi_new, kernel arguments) into a CUDA graph
+// and replayed with a single launch.  HSW_GRAPHS=0 disables.
+void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
+    if (time_it) CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+    const hsw_handle::GraphKey key{psi_old, psi_new, h->P.debug_flags, h->zero_pair, kernel_choice_for(h->S.dim, h->S.p)};
+    auto it = h->graphs.find(key);
+    if (!graphs_enabled() || (it == h->graphs.end() && !h->levels_configured)) {
+        h->last_launches = launch_all_levels(h, psi_old, psi_new);
+        h->levels_configured = true;
+    } else {
+        if (it == h->graphs.end()) {
+            cudaGraph_t g = nullptr;
+            CUDA_OK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+            int64_t launches = 0;
+            try {
+                launches = launch_all_levels(h, psi_old, psi_new);
+            } catch (...) {
+                cudaStreamEndCapture(h->stream, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            CUDA_OK(cudaStreamEndCapture(h->stream, &g));
+            cudaGraphExec_t ex = nullptr;
+            CUDA_OK(cudaGraphInstantiate(&ex, g, 0));
+            CUDA_OK(cudaGraphDestroy(g));
+            it = h->graphs.emplace(key, hsw_handle::GraphEntry{ex, launches}).first;
+        }
+        CUDA_OK(cudaGraphLaunch(it->second.exec, h->stream));
+        h->last_launches = it->second.launches;
+    }
     if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
-    h->last_launches = launches;
 }
 
 // Ordinate blocks of the pipelined host-pointer sweep: 4 when psi is large
