@@ -1458,7 +1458,7 @@ int kernel_choice_for(int dim, int p) {
     int env = kernel_choice_env();
     if (env == 3 && !dev_dmma1_supported(dim, p)) env = -1;
     if (env >= 0) return env;
-    if (dim == 3 && (p == 2 || p == 3)) return 3;
+    if ((dim == 3 || dim == 2) && (p == 2 || p == 3)) return 3;   // one-warp DMMA (measured fastest)
     return (dim == 3 && p >= 2) ? 1 : 2;
 }
 thread_local int g_kernel_dim = 2, g_kernel_p = 1;
