@@ -1362,6 +1362,9 @@ struct hsw_handle {
     };
     std::map<GraphKey, GraphEntry> graphs;
     bool levels_configured = false;
+    // dataflow schedule: per-pair completion flags (== epoch of the current sweep)
+    unsigned* d_done = nullptr;
+    unsigned epoch = 0;
     // host-pointer all-ordinate sweep: copy streams and per-block events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_sw;
@@ -1404,6 +1407,7 @@ void free_handle(hsw_handle* h) {
     for (auto& kv : h->ranges)
         if (kv.second.d_pairs) cudaFree(kv.second.d_pairs);
     for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (h->d_done) cudaFree(h->d_done);
     for (auto e : h->ev_in) cudaEventDestroy(e);
     for (auto e : h->ev_sw) cudaEventDestroy(e);
     for (auto e : h->ev_cp)
@@ -1425,6 +1429,17 @@ void need_device(const hsw_handle* h) {
 
 // Raise the first singular (element, ordinate) recorded by the kernels.
 void check_err(hsw_handle* h) {
+    if (h->d_done) {   // dataflow stall (see dmma1 kernel): results are invalid, fail loudly
+        unsigned stall = 0;
+        CUDA_OK(cudaMemcpyAsync(&stall, h->d_done + (size_t)h->S.nel * h->S.nd, sizeof(stall), cudaMemcpyDeviceToHost,
+                                h->stream));
+        CUDA_OK(cudaStreamSynchronize(h->stream));
+        if (stall) {
+            CUDA_OK(cudaMemsetAsync(h->d_done + (size_t)h->S.nel * h->S.nd, 0, sizeof(unsigned), h->stream));
+            throw hsw::Error(HSW_ERR_CUDA, "dataflow sweep stalled: the persistent CTAs were not all resident "
+                                           "(other work on the GPU?); set HSW_DATAFLOW=0");
+        }
+    }
     unsigned long long key = 0;
     CUDA_OK(cudaMemcpyAsync(&key, h->d_err, sizeof(key), cudaMemcpyDeviceToHost, h->stream));
     CUDA_OK(cudaStreamSynchronize(h->stream));
@@ -1492,12 +1507,53 @@ bool graphs_enabled() {
     return v;
 }
 
+// Dataflow schedule (HSW_DATAFLOW=1, one-warp DMMA kernel): the whole worklist
+// in one persistent launch; each pair waits for its retained upwind pairs'
+// completion flags instead of a per-level barrier.
+// Default: on for 3D (C3 -9 %, C4 -1.5 %), off for 2D (its 449 short levels are
+// faster level by level from a CUDA graph).  HSW_DATAFLOW=0/1 overrides.
+bool dataflow_enabled(const hsw_handle* h) {
+    static const int env = [] {
+        const char* e = std::getenv("HSW_DATAFLOW");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (kernel_choice_for(h->S.dim, h->S.p) != 3) return false;
+    return env >= 0 ? env == 1 : h->S.dim == 3;
+}
+
+unsigned next_epoch(hsw_handle* h) {
+    // flags [nel * nd] + one stall flag
+    const size_t bytes = ((size_t)h->S.nel * h->S.nd + 1) * sizeof(unsigned);
+    if (!h->d_done) {
+        CUDA_OK(cudaMalloc(&h->d_done, bytes));
+        CUDA_OK(cudaMemsetAsync(h->d_done, 0, bytes, h->stream));
+        h->epoch = 0;
+    }
+    if (++h->epoch == 0u) {   // wrapped: clear the flags
+        CUDA_OK(cudaMemsetAsync(h->d_done, 0, bytes, h->stream));
+        h->epoch = 1;
+    }
+    return h->epoch;
+}
+
+void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
+    const unsigned ep = next_epoch(h);
+    dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
+                    h->d_done, ep);
+}
+
 // The all-ordinate sweep is one launch per level (C2: 449 levels of ~24 us):
 // after a first direct run (which configures every kernel), the level sequence
 // is captured once per (psi_old, psi_new, kernel arguments) into a CUDA graph
 // and replayed with a single launch.  HSW_GRAPHS=0 disables.
 void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
     if (time_it) CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+    if (dataflow_enabled(h)) {
+        dataflow_sweep(h, psi_old, psi_new, h->d_pairs_all, (int)((size_t)h->S.nel * h->S.nd));
+        h->last_launches = 1;
+        if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+        return;
+    }
     const hsw_handle::GraphKey key{psi_old, psi_new, h->P.debug_flags, h->zero_pair, kernel_choice_for(h->S.dim, h->S.p)};
     auto it = h->graphs.find(key);
     if (!graphs_enabled() || (it == h->graphs.end() && !h->levels_configured)) {
@@ -1580,6 +1636,12 @@ const hsw_handle::RangeList& range_list(hsw_handle* h, int d0, int d1) {
 
 void run_range_levels(hsw_handle* h, const hsw_handle::RangeList& rl, const double* psi_old, double* psi_new) {
     CUDA_OK(cudaEventRecord(h->ev0, h->stream));
+    if (dataflow_enabled(h)) {   // the block's pairs depend only on pairs of the same ordinates
+        if (rl.offsets.back() > 0) dataflow_sweep(h, psi_old, psi_new, rl.d_pairs, rl.offsets.back());
+        CUDA_OK(cudaEventRecord(h->ev1, h->stream));
+        h->last_launches = 1;
+        return;
+    }
     int64_t launches = 0;
     for (size_t l = 0; l + 1 < rl.offsets.size(); ++l) {
         const int n = rl.offsets[l + 1] - rl.offsets[l];

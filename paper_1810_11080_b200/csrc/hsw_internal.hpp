@@ -110,8 +110,11 @@ void dev_phi_norms2(const DevProblem& P, const double* phi_new, const double* ph
                     void* stream);
 // one warp per pair, persistent, register + shared-memory DMMA tiles (hsw_dmma1.cu)
 bool dev_dmma1_supported(int dim, int p);
+// done_flags != nullptr: dataflow schedule over the whole worklist (one launch;
+// a pair waits for its retained upwind pairs' flags == epoch, then publishes its own)
 void dev_dmma1_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
-                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
+                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream,
+                     unsigned* done_flags = nullptr, unsigned epoch = 0);
 void dev_dmma1_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                            unsigned long long* err_key, int64_t zero_pair, void* stream);
 
