@@ -1522,8 +1522,8 @@ bool dataflow_enabled(const hsw_handle* h) {
 }
 
 unsigned next_epoch(hsw_handle* h) {
-    // flags [nel * nd] + one stall flag
-    const size_t bytes = ((size_t)h->S.nel * h->S.nd + 1) * sizeof(unsigned);
+    // flags [nel * nd] + the stall flag + the pair-claim counter
+    const size_t bytes = ((size_t)h->S.nel * h->S.nd + 2) * sizeof(unsigned);
     if (!h->d_done) {
         CUDA_OK(cudaMalloc(&h->d_done, bytes));
         CUDA_OK(cudaMemsetAsync(h->d_done, 0, bytes, h->stream));
@@ -1538,6 +1538,7 @@ unsigned next_epoch(hsw_handle* h) {
 
 void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
     const unsigned ep = next_epoch(h);
+    CUDA_OK(cudaMemsetAsync(h->d_done + (size_t)h->S.nel * h->S.nd + 1, 0, sizeof(unsigned), h->stream));
     dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
                     h->d_done, ep);
 }
