@@ -362,7 +362,9 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             tj = json.load(open(prof))
-            if "dram_bytes_per_pair" in tj:   # ncu capture of one level, scaled to the average launch
+            if "dram_bytes_per_sweep" in tj:   # ncu over a whole sweep, per sweep-kernel launch
+                traffic = tj["dram_bytes_per_sweep"] * (pairs_rank / pairs) / max(launches_per_step - 1, 1)
+            elif "dram_bytes_per_pair" in tj:   # ncu capture of one level, scaled to the average launch
                 traffic = tj["dram_bytes_per_pair"] * pairs_rank / max(launches_per_step - 1, 1)
             else:
                 traffic = tj.get("dram_bytes_per_launch")
