@@ -240,6 +240,15 @@ int hsw_debug_flags(hsw_handle* h, int flags);
  * elimination, write-back, pair count; 8-11: panel wait, U, DMMA, factor). */
 int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]);
 
+/* Test hook: the library's graph ordering (Tarjan SCC, exact FAS DP for SCCs
+ * <= threshold else the weighted Eades-Lin-Smyth heuristic, min-heap Kahn on
+ * the condensation; sweepgraph.hpp:54-396) on an arbitrary digraph with
+ * edges[2*ne] (from, to) and weights[ne]; writes order[nv], lagged[<= ne]
+ * (edge ids, ascending) and the cut weight.  Returns the number of lagged
+ * edges, or a negative status. */
+int hsw_debug_graph_order(int nv, int ne, const int* edges, const double* weights, int threshold, int* order,
+                          int* lagged, double* lagged_weight);
+
 /* Test hook mirroring test_solver.cpp:332-344 (op.ordinates[d].diag[e].setZero()):
  * zero the assembled local block of (e, d) in every later factorization. */
 int hsw_debug_zero_block(hsw_handle* h, int e, int d);

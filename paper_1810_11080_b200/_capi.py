@@ -29,7 +29,7 @@ EXPORTED = [
     "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
     "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
     "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_phi_partial", "hsw_shard_psi_error",
-    "hsw_shard_phi_norms", "hsw_shard_advance", "hsw_shard_psi",
+    "hsw_shard_phi_norms", "hsw_shard_advance", "hsw_shard_psi", "hsw_debug_graph_order",
 ]
 
 
@@ -106,6 +106,7 @@ def load():
     L.hsw_shard_phi_norms.argtypes = [vp, vp, vp, vp]
     L.hsw_shard_advance.argtypes = [vp, vp]
     L.hsw_shard_psi.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.hsw_debug_graph_order.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, vp, C.POINTER(C.c_double)]
     _lib = L
     return L
 

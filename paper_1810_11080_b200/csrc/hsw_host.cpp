@@ -2401,6 +2401,32 @@ int hsw_fp64_peak(int device, double* tflops) {
     });
 }
 
+// Test hook: the product's graph ordering (Tarjan + exact/heuristic FAS + min-heap
+// Kahn, sweepgraph.hpp:318-396) on an arbitrary weighted digraph, for randomized
+// bit-exactness tests against the oracle.  Returns the number of lagged edges.
+int hsw_debug_graph_order(int nv, int ne, const int* edges, const double* weights, int threshold, int* order,
+                          int* lagged, double* lagged_weight) {
+    try {
+        if (nv < 1 || ne < 0 || (ne > 0 && (!edges || !weights)) || !order)
+            throw hsw::Error(HSW_ERR_INVALID, "hsw_debug_graph_order: bad arguments");
+        std::vector<Edge> es((size_t)ne);
+        for (int i = 0; i < ne; ++i) {
+            if (edges[2 * i] < 0 || edges[2 * i] >= nv || edges[2 * i + 1] < 0 || edges[2 * i + 1] >= nv)
+                throw hsw::Error(HSW_ERR_RANGE, "hsw_debug_graph_order: vertex out of range");
+            es[i] = {edges[2 * i], edges[2 * i + 1], weights[i]};
+        }
+        const Ordering o = sweep_ordering(nv, es, threshold);
+        std::copy(o.order.begin(), o.order.end(), order);
+        if (lagged) std::copy(o.lagged_edges.begin(), o.lagged_edges.end(), lagged);
+        if (lagged_weight) *lagged_weight = o.lagged_weight;
+        return (int)o.lagged_edges.size();
+    } catch (const hsw::Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::exception& e) {
+        return fail(HSW_ERR_LOGIC, e.what());
+    }
+}
+
 int hsw_debug_flags(hsw_handle* h, int flags) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_debug_flags: null handle");
     h->P.debug_flags = flags;
