@@ -364,30 +364,48 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
 
     // pivot search on a candidate column (this warp's copy of the rows)
     auto search = [&](const double (&cv)[R], double (&lo)[R], int& prow_o, double& piv_o) {
-        unsigned key = 0u;
-        int ks = 0;
-        double cm = cv[0];
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            // high word of |a| + 1: every unpivoted row is a candidate, ties -> lowest lane
-            const unsigned hi = (unsigned)(__double_as_longlong(fabs(cv[i])) >> 32) + 1u;
-            if (!((done >> i) & 1u) && hi > key) { key = hi; ks = i; cm = cv[i]; }
-        }
-        unsigned kmax;
         if (PPW == 1) {
-            kmax = __reduce_max_sync(0xffffffffu, key);
+            // one packed key per lane [|a| high word >> KLB, + 1][row slot][31 - lane]
+            // (pivoted rows 0): a single redux.max yields the pivot row; pivot chosen
+            // within 2^-14 of max |a| (ties -> higher slot, then lower lane)
+            constexpr int KLB = 5 + (R <= 1 ? 0 : R <= 2 ? 1 : R <= 4 ? 2 : 3);
+            unsigned key = 0u;
+            int ks = 0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const unsigned hi = (unsigned)(__double_as_longlong(cv[i]) >> 32) & 0x7fffffffu;
+                const unsigned kk = ((((hi >> KLB) + 1u) << KLB) | ((unsigned)i << 5) | (31u - ll));
+                if (!((done >> i) & 1u) && kk > key) { key = kk; ks = i; }
+            }
+            double cm = cv[0];
+#pragma unroll
+            for (int i = 1; i < R; ++i)
+                if (i == ks) cm = cv[i];
+            const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+            const int src_lane = 31 - (int)(kmax & 31u);
+            prow_o = src_lane + 32 * (int)((kmax >> 5) & ((1u << (KLB - 5)) - 1u));
+            piv_o = __shfl_sync(0xffffffffu, cm, src_lane);
         } else {
-            kmax = 0u;
+            unsigned key = 0u;
+            int ks = 0;
+            double cm = cv[0];
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                // high word of |a| + 1: every unpivoted row is a candidate, ties -> lowest lane
+                const unsigned hi = (unsigned)(__double_as_longlong(fabs(cv[i])) >> 32) + 1u;
+                if (!((done >> i) & 1u) && hi > key) { key = hi; ks = i; cm = cv[i]; }
+            }
+            unsigned kmax = 0u;
 #pragma unroll
             for (int pp = 0; pp < PPW; ++pp) {
                 const unsigned t = __reduce_max_sync(0xffffffffu, ps == pp ? key : 0u);
                 if (ps == pp) kmax = t;
             }
+            const unsigned bal = __ballot_sync(0xffffffffu, key == kmax && key != 0u) & gbits;
+            const int src_lane = __ffs(bal) - 1;
+            prow_o = __shfl_sync(0xffffffffu, ll + L * ks, src_lane);
+            piv_o = __shfl_sync(0xffffffffu, cm, src_lane);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, key == kmax && key != 0u) & gbits;
-        const int src_lane = __ffs(bal) - 1;
-        prow_o = __shfl_sync(0xffffffffu, ll + L * ks, src_lane);
-        piv_o = __shfl_sync(0xffffffffu, cm, src_lane);
         if (!(fabs(piv_o) > 1e-14 * amax)) singular = true;
         const double rinv = 1.0 / piv_o;
 #pragma unroll
@@ -408,7 +426,7 @@ gj_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const doubl
         }
     };
     auto consume = [&](int k, double (&lo)[R], int& prow_o, double& piv_o) {
-        while (*ready < k) __nanosleep(32);
+        while (*ready < k) __nanosleep(8);
         __threadfence_block();
         const double* slot = ring + (k & 7) * RS;
 #pragma unroll
