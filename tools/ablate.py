@@ -26,3 +26,15 @@ n = max(int(out[5]), 1)
 names = ["tables", "faces", "assembly", "elimination", "writeback"]
 print(name, "pairs", n, " ".join(f"{nm}={int(out[i])/n:.0f}cyc" for i, nm in enumerate(names)), flush=True)
 print(name, "panel loop:", " ".join(f"{nm}={int(out[8 + i])/n:.0f}cyc" for i, nm in enumerate([os.environ.get("P8", "wait"), os.environ.get("P9", "U"), "dmma", "factor"])), flush=True)
+print(name, "volume split: register tiles", int(out[6]) // n, "cyc, TMEM tiles", int(out[7]) // n, "cyc", flush=True)
+
+for extra in (16, 32):   # only warp 0 / warps 0-3 per CTA work: the single-warp latency of each phase
+    L.hsw_debug_flags(s.handle, 8 | extra)
+    L.hsw_sweep_resident(s.handle); L.hsw_synchronize(s.handle)
+    ms = L.hsw_last_sweep_kernel_ms(s.handle)
+    d = np.zeros(16, np.uint64)
+    L.hsw_debug_profile(s.handle, C.c_void_p(d.ctypes.data))
+    n2 = max(int(d[5]), 1)
+    print(name, f"flags 8|{extra}: sweep {ms:.1f} ms, pairs {n2}", " ".join(f"{nm}={int(d[i])/n2:.0f}" for i, nm in enumerate(names)),
+          "| factor", int(d[11]) // n2, "gather", int(d[8]) // n2, "update", int(d[9]) // n2, "volT", int(d[7]) // n2,
+          "| factor: load", int(d[12]) // n2, "steps", int(d[13]) // n2, "| gather TMEM+reg", int(d[14]) // n2, flush=True)
