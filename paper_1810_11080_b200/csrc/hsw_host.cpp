@@ -1322,6 +1322,7 @@ struct hsw_handle {
     DevProblem P{};
     // device buffers
     double *d_T = nullptr, *d_sig_t = nullptr, *d_sig_s = nullptr, *d_qvol = nullptr, *d_fgeom = nullptr;
+    double* d_bscale = nullptr;
     int* d_fnbr = nullptr;
     uint16_t* d_inflags = nullptr;
     double *d_omega = nullptr, *d_weight = nullptr;
@@ -1398,7 +1399,7 @@ T* dev_upload(const std::vector<T>& v) {
 
 void free_handle(hsw_handle* h) {
     if (!h) return;
-    void* bufs[] = {h->d_T, h->d_sig_t, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
+    void* bufs[] = {h->d_T, h->d_sig_t, h->d_bscale, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
                     h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
                     h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
@@ -1841,6 +1842,8 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         }
         h->d_sig_t = dev_upload(S.sig_t);
         h->d_sig_s = dev_upload(S.sig_s);
+        CUDA_OK(cudaMalloc(&h->d_bscale, (size_t)S.nel * sizeof(double)));
+        dev_block_scale(S.nel, S.nb, h->d_T, h->d_sig_t, h->d_bscale, h->stream);
         h->d_fgeom = dev_upload(S.fgeom);
         h->d_fnbr = dev_upload(S.fnbr);
         h->d_inflags = dev_upload(S.inflags);
@@ -1875,7 +1878,7 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         DevProblem& P = h->P;
         P.dim = S.dim; P.p = S.p; P.nb = S.nb; P.nfn = S.nfn; P.nqf = S.nqf; P.nfaces = S.nf;
         P.nel = S.nel; P.nd = S.nd;
-        P.T = h->d_T; P.sig_t = h->d_sig_t; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
+        P.T = h->d_T; P.sig_t = h->d_sig_t; P.bscale = h->d_bscale; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
         P.fgeom = h->d_fgeom; P.fnbr = h->d_fnbr; P.inflags = h->d_inflags;
         P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;
         P.g_fnode = h->d_tab_fnode; P.g_trace = h->d_tab_trace; P.g_fidx = h->d_tab_fidx;

@@ -27,6 +27,8 @@ struct DevProblem {
                               // with G_k = -(d_k u)^T W u
     const double* sig_t;      // [E]
     const double* sig_s;      // [E]
+    const double* bscale;     // [E] max_ij (sig_t |M| + |Gx| + |Gy| + |Gz|)_ij >= max |volume part of A(Omega)|:
+                              //     the matrix scale of the singular-block test (dmma1 kernel)
     const double* qvol;       // [E][nb] volume source moments
     const double* fgeom;      // [E][nfaces][nqf][4]: outward normal (own side), w_q*|J_Gamma|
     const int* fnbr;          // [E][nfaces][4]: neighbour elem (-1 boundary), neighbour face,
@@ -94,6 +96,7 @@ void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_ol
 void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                           unsigned long long* err_key, int64_t zero_pair, void* stream);
 // device-side setup (hsw_setup.cu): element tensors + volume source moments, absorption
+void dev_block_scale(int nel, int nb, const double* T, const double* sig_t, double* out, void* stream);
 void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double* pts, const int* enodes,
                          const double* U, const double* DU, const double* GG, const double* GV, const double* wq,
                          int source_kind, const SourceParams& sp, double* T, double* qvol,

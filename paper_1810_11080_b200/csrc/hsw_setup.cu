@@ -171,7 +171,35 @@ absorption_kernel(int nel, int nb, const double* __restrict__ T, const double* _
     if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
+// per element: max over the n x n entries of sig_t |M| + |Gx| + |Gy| + |Gz| (an
+// ordinate-independent upper bound of max |sigma_t M + sum_k Omega_k G_k|, |Omega_k| <= 1)
+__global__ void __launch_bounds__(kSetupThreads) block_scale_kernel(int nb, const double* __restrict__ T,
+                                                                    const double* __restrict__ sig_t,
+                                                                    double* __restrict__ out) {
+    __shared__ double red[kSetupThreads];
+    const int e = blockIdx.x;
+    const double st = sig_t[e];
+    const double4* Te = reinterpret_cast<const double4*>(T) + (size_t)e * nb * nb;
+    double m = 0.0;
+    for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) {
+        const double4 t = Te[i];
+        m = fmax(m, st * fabs(t.x) + fabs(t.y) + fabs(t.z) + fabs(t.w));
+    }
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[e] = red[0];
+}
+
 }  // namespace
+
+void dev_block_scale(int nel, int nb, const double* T, const double* sig_t, double* out, void* stream) {
+    block_scale_kernel<<<nel, kSetupThreads, 0, (cudaStream_t)stream>>>(nb, T, sig_t, out);
+    SCHECK(cudaGetLastError());
+}
 
 void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double* pts, const int* enodes,
                          const double* U, const double* DU, const double* GG, const double* GV, const double* wq,
