@@ -334,7 +334,8 @@ def run_ours(args):
             psi_old_h = torch.zeros((nd, N), dtype=torch.float64).pin_memory()
             psi_new_h = torch.empty((nd, N), dtype=torch.float64).pin_memory()
             for _ in range(1):
-                assert L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr())) == 0
+                rc = L.hsw_sweep(h, -1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()), vp(psi_new_h.data_ptr()))
+                assert rc == 0, _capi.last_error()
             e2e_steps = max(1, min(args.steps, 3))
             barrier()
             t0 = time.perf_counter()
