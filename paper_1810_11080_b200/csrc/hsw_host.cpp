@@ -2033,6 +2033,8 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
                 // psi_old (lagged couplings stay within an ordinate), so the H2D of
                 // block b+1 and the D2H of block b-1 overlap the sweep of block b.
                 ensure_copy_streams(h, nblk);
+                for (int b = 0; b < nblk; ++b)   // worklists first: no allocation / sync copy between launches
+                    (void)range_list(h, (int)((int64_t)b * nd / nblk), (int)((int64_t)(b + 1) * nd / nblk));
                 CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
                 CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
                 dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
