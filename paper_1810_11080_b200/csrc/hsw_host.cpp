@@ -1588,13 +1588,27 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
 
 // Ordinate blocks of the pipelined host-pointer sweep: 4 when psi is large
 // enough for PCIe time to matter (HSW_E2E_BLOCKS overrides; 1 disables).
-int e2e_blocks(const hsw_handle* h) {
+int e2e_blocks_env() {
     static const int env = [] {
         const char* v = std::getenv("HSW_E2E_BLOCKS");
         return v ? std::atoi(v) : 0;
     }();
-    int b = env > 0 ? env : ((double)h->N * h->S.nd * sizeof(double) >= 64e6 ? 4 : 1);
+    return env;
+}
+int e2e_blocks(const hsw_handle* h) {
+    const int env = e2e_blocks_env();
+    int b = env > 0 ? env : ((double)h->N * h->S.nd * sizeof(double) >= 64e6 ? 6 : 1);
     return std::max(1, std::min(b, h->S.nd));
+}
+// First ordinate of block b (of nblk).  Default (no HSW_E2E_BLOCKS, >= 32 ordinates):
+// a ramp of relative sizes 1:3:8:12:6:2, so that only a small first block's H2D and a
+// small last block's D2H stay exposed while every other transfer hides behind a
+// larger neighbouring sweep (the copies run ~5x faster per ordinate than the sweep).
+int e2e_block_start(const hsw_handle* h, int b, int nblk) {
+    const int nd = h->S.nd;
+    static const int ramp[7] = {0, 1, 4, 12, 24, 30, 32};
+    if (e2e_blocks_env() > 0 || nblk != 6 || nd < 32) return (int)((int64_t)b * nd / nblk);
+    return (int)((int64_t)ramp[b] * nd / 32);
 }
 
 void ensure_copy_streams(hsw_handle* h, int nblk) {
@@ -2034,18 +2048,18 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
                 // block b+1 and the D2H of block b-1 overlap the sweep of block b.
                 ensure_copy_streams(h, nblk);
                 for (int b = 0; b < nblk; ++b)   // worklists first: no allocation / sync copy between launches
-                    (void)range_list(h, (int)((int64_t)b * nd / nblk), (int)((int64_t)(b + 1) * nd / nblk));
+                    (void)range_list(h, e2e_block_start(h, b, nblk), e2e_block_start(h, b + 1, nblk));
                 CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
                 CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
                 dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
                 for (int b = 0; b < nblk; ++b) {
-                    const int d0 = (int)((int64_t)b * nd / nblk), d1 = (int)((int64_t)(b + 1) * nd / nblk);
+                    const int d0 = e2e_block_start(h, b, nblk), d1 = e2e_block_start(h, b + 1, nblk);
                     const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
                     CUDA_OK(cudaMemcpyAsync(h->d_psiA + off, psi_old + off, cnt, cudaMemcpyHostToDevice, h->copy_in));
                     CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
                 }
                 for (int b = 0; b < nblk; ++b) {
-                    const int d0 = (int)((int64_t)b * nd / nblk), d1 = (int)((int64_t)(b + 1) * nd / nblk);
+                    const int d0 = e2e_block_start(h, b, nblk), d1 = e2e_block_start(h, b + 1, nblk);
                     const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
                     CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
                     run_range_levels(h, range_list(h, d0, d1), h->d_psiA, h->d_psiB);
