@@ -234,10 +234,15 @@ int hsw_shard_psi(hsw_handle* h, int d0, int d1, double* psi);
 int hsw_fp64_peak(int device, double* tflops);
 
 /* Ablation switches for development timing (results are NOT valid solves):
- * 1 skip the face terms, 2 skip the elimination, 4 skip the tensor loads. */
+ * 1 skip the face terms, 2 skip the elimination, 4 skip the tensor loads,
+ * 8 phase clocks, 16 / 32 only warp 0 / warps 0-3 of each CTA work.  Honoured
+ * by the one-warp DMMA kernel's profiling instantiations (3D Q3 and Q4); the
+ * production kernels carry no debug code. */
 int hsw_debug_flags(hsw_handle* h, int flags);
-/* Debug phase-cycle counters of flag 8 (table staging, faces, assembly,
- * elimination, write-back, pair count; 8-11: panel wait, U, DMMA, factor). */
+/* Debug phase-cycle counters of flag 8 (0-5: volume, faces, assembly,
+ * elimination, write-back, pair count; 6-7: register / TMEM volume parts;
+ * 8-11: pivot-row gather, update, dependency wait, factor; 12-14: factor
+ * load, pivot steps, gather TMEM + register part). */
 int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]);
 
 /* Test hook: the library's graph ordering (Tarjan SCC, exact FAS DP for SCCs

@@ -44,8 +44,9 @@ struct DevProblem {
     const int* g_nmask;       // [128]
     const double* g_line;     // [8][8]
     int debug_flags;          // ablation (tools/ablate.py): 1 skip faces, 2 skip elimination, 4 skip T loads,
-                              // 8 per-phase clock64 counters into prof[]
-    unsigned long long* prof; // [8] debug phase-cycle accumulators
+                              // 8 per-phase clock64 counters into prof[], 16/32 warp subsets (dmma1
+                              // profiling instantiations only)
+    unsigned long long* prof; // [16] debug phase-cycle accumulators
 };
 
 // Host-computed tables that are uploaded to constant memory.
