@@ -306,18 +306,22 @@ def run_ours(args):
             vp = C.c_void_p
 
             def e2e_step():
-                cu = torch.cuda.current_stream()
-                pa2, pb2, ph2 = C.c_void_p(), C.c_void_p(), C.c_void_p()
-                L.hsw_device_state(h, C.byref(pa2), C.byref(pb2), C.byref(ph2))
-                dev_old = _DevView(pa2.value + d0 * N * 8, (nb, N))
-                torch.as_tensor(dev_old, device=f"cuda:{local}").copy_(psi_old_h, non_blocking=True)
-                phi_t.copy_(phi_h, non_blocking=True)
-                cu.synchronize()
-                step()
-                L.hsw_synchronize(h)
-                dev_new = _DevView(pb2.value + d0 * N * 8, (nb, N))
-                psi_new_h.copy_(torch.as_tensor(dev_new, device=f"cuda:{local}"), non_blocking=True)
-                cu.synchronize()
+                # block sweep with host buffers (H2D / sweep / D2H pipelined over sub-blocks),
+                # then the chained phi over the ranks as in step()
+                rc = L.hsw_shard_sweep_host(h, d0, d1, vp(phi_h.data_ptr()), vp(psi_old_h.data_ptr()),
+                                            vp(psi_new_h.data_ptr()))
+                assert rc == 0, _capi.last_error()
+                prefix = None
+                if world > 1 and rank > 0:
+                    prefix = be.zeros()
+                    torch.distributed.recv(prefix, src=rank - 1)
+                out = be.zeros()
+                be.phi_partial(d0, d1, prefix, out)
+                if world > 1:
+                    if rank < world - 1:
+                        torch.distributed.send(out, dst=rank + 1)
+                    torch.distributed.broadcast(out, src=world - 1)
+                torch.cuda.current_stream().synchronize()
 
             e2e_step()
             e2e_steps = max(1, min(args.steps, 3))
@@ -328,7 +332,7 @@ def run_ours(args):
             barrier()
             e2e_s = (time.perf_counter() - t0) / e2e_steps
             h2d, d2h = (nd * N + world * N) * 8, nd * N * 8
-            api = "per rank: psi_old block + phi H2D, hsw_shard_sweep + chained phi (NCCL), psi_new block D2H"
+            api = "per rank: hsw_shard_sweep_host (psi_old block + phi H2D, pipelined block sweep, psi_new block D2H) + chained phi (NCCL)"
         else:
             phi_h = torch.full((N,), 0.1, dtype=torch.float64).pin_memory()
             psi_old_h = torch.zeros((nd, N), dtype=torch.float64).pin_memory()

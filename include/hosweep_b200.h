@@ -212,6 +212,11 @@ int hsw_shard_reset(hsw_handle* h);
  * the block's own retained upwind values.  Worklist: the block's pairs sorted
  * by (level, element, ordinate), built once per block and cached. */
 int hsw_shard_sweep(hsw_handle* h, int d0, int d1, const double* phi_dev);
+/* The same block sweep end to end with HOST buffers: phi (N doubles) and the
+ * block's psi_old / psi_new ((d1 - d0) x N, row d - d0), H2D / sweep / D2H
+ * pipelined over ordinate sub-blocks as in hsw_sweep(d = -1); the block's
+ * psi_new also stays on the device for hsw_shard_phi_partial.  Synchronous. */
+int hsw_shard_sweep_host(hsw_handle* h, int d0, int d1, const double* phi, const double* psi_old, double* psi_new);
 /* out_dev = prefix_dev + sum_{d0 <= d < d1} w_d psi_new_d, accumulated per
  * (e, m) in ascending d with one FMA per ordinate (prefix_dev NULL: 0).
  * Chaining blocks in rank order reproduces hsw_source_iteration's phi bit for

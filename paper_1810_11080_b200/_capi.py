@@ -28,7 +28,7 @@ EXPORTED = [
     "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
     "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
     "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
-    "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_phi_partial", "hsw_shard_psi_error",
+    "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_sweep_host", "hsw_shard_phi_partial", "hsw_shard_psi_error",
     "hsw_shard_phi_norms", "hsw_shard_advance", "hsw_shard_psi", "hsw_debug_graph_order",
 ]
 
@@ -101,6 +101,7 @@ def load():
     L.hsw_debug_profile.argtypes = [vp, vp]
     L.hsw_shard_reset.argtypes = [vp]
     L.hsw_shard_sweep.argtypes = [vp, C.c_int, C.c_int, vp]
+    L.hsw_shard_sweep_host.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
     L.hsw_shard_phi_partial.argtypes = [vp, C.c_int, C.c_int, vp, vp]
     L.hsw_shard_psi_error.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double)]
     L.hsw_shard_phi_norms.argtypes = [vp, vp, vp, vp]

@@ -1595,20 +1595,19 @@ int e2e_blocks_env() {
     }();
     return env;
 }
-int e2e_blocks(const hsw_handle* h) {
+int e2e_blocks(const hsw_handle* h, int nr) {   // nr: ordinates of the swept range
     const int env = e2e_blocks_env();
-    int b = env > 0 ? env : ((double)h->N * h->S.nd * sizeof(double) >= 64e6 ? 6 : 1);
-    return std::max(1, std::min(b, h->S.nd));
+    int b = env > 0 ? env : ((double)h->N * nr * sizeof(double) >= 64e6 ? 6 : 1);
+    return std::max(1, std::min(b, nr));
 }
 // First ordinate of block b (of nblk).  Default (no HSW_E2E_BLOCKS, >= 32 ordinates):
 // a ramp of relative sizes 1:3:8:12:6:2, so that only a small first block's H2D and a
 // small last block's D2H stay exposed while every other transfer hides behind a
 // larger neighbouring sweep (the copies run ~5x faster per ordinate than the sweep).
-int e2e_block_start(const hsw_handle* h, int b, int nblk) {
-    const int nd = h->S.nd;
+int e2e_block_start(int b, int nblk, int nr) {   // offset within a range of nr ordinates
     static const int ramp[7] = {0, 1, 4, 12, 24, 30, 32};
-    if (e2e_blocks_env() > 0 || nblk != 6 || nd < 32) return (int)((int64_t)b * nd / nblk);
-    return (int)((int64_t)ramp[b] * nd / 32);
+    if (e2e_blocks_env() > 0 || nblk != 6 || nr < 32) return (int)((int64_t)b * nr / nblk);
+    return (int)((int64_t)ramp[b] * nr / 32);
 }
 
 void ensure_copy_streams(hsw_handle* h, int nblk) {
@@ -2027,6 +2026,52 @@ int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* 
     });
 }
 
+// Sweep of ordinates [r0, r1) with HOST psi buffers holding that range (row d - r0),
+// from the scattering source of h->d_phi_old.  Pipelined over ordinate blocks: a
+// block's sweep needs only its own psi_old (lagged couplings stay within an
+// ordinate), so the H2D of block b+1 and the D2H of block b-1 overlap the sweep of
+// block b.  Stream-ordered on h->stream (the caller synchronizes).
+static void pipelined_range_sweep(hsw_handle* h, int r0, int r1, const double* psi_old, double* psi_new) {
+    const size_t N = h->N;
+    const int nr = r1 - r0;
+    const int nblk = e2e_blocks(h, nr);
+    if (nblk <= 1) {
+        CUDA_OK(cudaMemcpyAsync(h->d_psiA + (size_t)r0 * N, psi_old, N * nr * sizeof(double), cudaMemcpyHostToDevice,
+                                h->stream));
+        dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+        if (r0 == 0 && r1 == h->S.nd)
+            run_all_levels(h, h->d_psiA, h->d_psiB, false);
+        else
+            run_range_levels(h, range_list(h, r0, r1), h->d_psiA, h->d_psiB);
+        CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB + (size_t)r0 * N, N * nr * sizeof(double), cudaMemcpyDeviceToHost,
+                                h->stream));
+        return;
+    }
+    ensure_copy_streams(h, nblk);
+    for (int b = 0; b < nblk; ++b)   // worklists first: no allocation / sync copy between launches
+        (void)range_list(h, r0 + e2e_block_start(b, nblk, nr), r0 + e2e_block_start(b + 1, nblk, nr));
+    CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
+    CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
+    dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+    for (int b = 0; b < nblk; ++b) {
+        const int d0 = r0 + e2e_block_start(b, nblk, nr), d1 = r0 + e2e_block_start(b + 1, nblk, nr);
+        const size_t off = (size_t)d0 * N, hoff = (size_t)(d0 - r0) * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
+        CUDA_OK(cudaMemcpyAsync(h->d_psiA + off, psi_old + hoff, cnt, cudaMemcpyHostToDevice, h->copy_in));
+        CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
+    }
+    for (int b = 0; b < nblk; ++b) {
+        const int d0 = r0 + e2e_block_start(b, nblk, nr), d1 = r0 + e2e_block_start(b + 1, nblk, nr);
+        const size_t off = (size_t)d0 * N, hoff = (size_t)(d0 - r0) * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
+        CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
+        run_range_levels(h, range_list(h, d0, d1), h->d_psiA, h->d_psiB);
+        CUDA_OK(cudaEventRecord(h->ev_sw[b], h->stream));
+        CUDA_OK(cudaStreamWaitEvent(h->copy_out, h->ev_sw[b], 0));
+        CUDA_OK(cudaMemcpyAsync(psi_new + hoff, h->d_psiB + off, cnt, cudaMemcpyDeviceToHost, h->copy_out));
+    }
+    CUDA_OK(cudaEventRecord(h->ev_cp[1], h->copy_out));
+    CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_cp[1], 0));
+}
+
 int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, double* psi_new) {
     return guarded([&] {
         if (!h || !phi || !psi_old || !psi_new) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep: null argument");
@@ -2035,41 +2080,7 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
         const size_t N = h->N;
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         if (d == -1) {
-            const int nd = h->S.nd;
-            const int nblk = e2e_blocks(h);
-            if (nblk <= 1) {
-                CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi_old, N * nd * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-                dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
-                run_all_levels(h, h->d_psiA, h->d_psiB, false);
-                CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB, N * nd * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-            } else {
-                // Pipelined over ordinate blocks: a block's sweep needs only its own
-                // psi_old (lagged couplings stay within an ordinate), so the H2D of
-                // block b+1 and the D2H of block b-1 overlap the sweep of block b.
-                ensure_copy_streams(h, nblk);
-                for (int b = 0; b < nblk; ++b)   // worklists first: no allocation / sync copy between launches
-                    (void)range_list(h, e2e_block_start(h, b, nblk), e2e_block_start(h, b + 1, nblk));
-                CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
-                CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
-                dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
-                for (int b = 0; b < nblk; ++b) {
-                    const int d0 = e2e_block_start(h, b, nblk), d1 = e2e_block_start(h, b + 1, nblk);
-                    const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
-                    CUDA_OK(cudaMemcpyAsync(h->d_psiA + off, psi_old + off, cnt, cudaMemcpyHostToDevice, h->copy_in));
-                    CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
-                }
-                for (int b = 0; b < nblk; ++b) {
-                    const int d0 = e2e_block_start(h, b, nblk), d1 = e2e_block_start(h, b + 1, nblk);
-                    const size_t off = (size_t)d0 * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
-                    CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
-                    run_range_levels(h, range_list(h, d0, d1), h->d_psiA, h->d_psiB);
-                    CUDA_OK(cudaEventRecord(h->ev_sw[b], h->stream));
-                    CUDA_OK(cudaStreamWaitEvent(h->copy_out, h->ev_sw[b], 0));
-                    CUDA_OK(cudaMemcpyAsync(psi_new + off, h->d_psiB + off, cnt, cudaMemcpyDeviceToHost, h->copy_out));
-                }
-                CUDA_OK(cudaEventRecord(h->ev_cp[1], h->copy_out));
-                CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_cp[1], 0));
-            }
+            pipelined_range_sweep(h, 0, h->S.nd, psi_old, psi_new);
         } else {
             double* slotA = h->d_psiA + (size_t)d * N;
             double* slotB = h->d_psiB + (size_t)d * N;
@@ -2308,6 +2319,19 @@ int hsw_shard_reset(hsw_handle* h) {
         CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
         CUDA_OK(cudaMemsetAsync(h->d_psiB, 0, N * nd * sizeof(double), h->stream));
         CUDA_OK(cudaMemsetAsync(h->d_phi, 0, N * sizeof(double), h->stream));
+        return HSW_OK;
+    });
+}
+
+int hsw_shard_sweep_host(hsw_handle* h, int d0, int d1, const double* phi, const double* psi_old, double* psi_new) {
+    return guarded([&] {
+        if (!h || !phi || !psi_old || !psi_new) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_sweep_host: null argument");
+        need_device(h);
+        check_block(h, d0, d1, "hsw_shard_sweep_host");
+        CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        pipelined_range_sweep(h, d0, d1, psi_old, psi_new);
+        h->last_launches += 1;
+        check_err(h);
         return HSW_OK;
     });
 }
