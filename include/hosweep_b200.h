@@ -6,8 +6,10 @@
  * assembly.hpp:333-409).  Plain C: POD structs, pointers + sizes, int status
  * codes, no exceptions and no torch/Eigen types.  One handle owns the device
  * state of one assembled problem; calls on a handle are stream-ordered on the
- * handle's CUDA stream and not thread-safe with each other (use one handle per
- * host thread, like SweepSolver's const methods used per ordinate).
+ * handle's CUDA stream, serialised by a per-handle lock (so a reference-style
+ * parallel_for over ordinates calling sweep(d) concurrently is safe,
+ * solver.hpp:145-149) and run on the handle's device whatever device is
+ * current on the calling thread (restored on return).
  *
  * Error model: every call returns HSW_OK (0) or a negative status; the message
  * of the last failure on the calling thread is available from hsw_last_error()
@@ -28,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HSW_ABI_VERSION 1
+#define HSW_ABI_VERSION 2
 
 enum hsw_status {
     HSW_OK = 0,
@@ -169,9 +171,13 @@ int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* 
 int hsw_direct_oracle(hsw_handle* h, int d, const double* phi, double* psi);
 
 /* SweepSolver::source_iteration (solver.hpp:136-168).  psi_out ([nd][N]) and
- * phi_out (N) may be NULL; err_hist / phi_hist (max_iterations) may be NULL. */
+ * phi_out (N) may be NULL; err_hist / phi_hist (max_iterations) may be NULL;
+ * per_ordinate_hist ([max_iterations][nd], may be NULL) receives
+ * ConvergenceHistory::per_ordinate, error[it][d] = ||dpsi_d||_inf
+ * (solver.hpp:36,150-156). */
 int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_result* res,
-                         double* psi_out, double* phi_out, double* err_hist, double* phi_hist);
+                         double* psi_out, double* phi_out, double* err_hist, double* phi_hist,
+                         double* per_ordinate_hist);
 
 /* balance_report (solver.hpp:220-245) on a state; out5 = source_volume,
  * inflow, absorption, outflow, residual; attrs/vals: outflow by boundary
@@ -258,6 +264,11 @@ int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]);
  * edges, or a negative status. */
 int hsw_debug_graph_order(int nv, int ne, const int* edges, const double* weights, int threshold, int* order,
                           int* lagged, double* lagged_weight);
+
+/* Test hook mirroring test_solver.cpp:332-344 for the constructor check: the
+ * next hsw_create on the calling thread zeroes the (e, d) local block from the
+ * start, so check_local_blocks reports it as SolverError at construction. */
+int hsw_debug_create_zero_block(int e, int d);
 
 /* Test hook mirroring test_solver.cpp:332-344 (op.ordinates[d].diag[e].setZero()):
  * zero the assembled local block of (e, d) in every later factorization. */

@@ -10,6 +10,7 @@
 #include "hosweep_b200.h"
 
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -67,8 +68,9 @@ struct SweepOrdering {
 };
 
 struct ConvergenceHistory {  // solver.hpp:34-39
-    std::vector<double> error;    // per iteration, max over ordinates of ||dpsi||_inf
-    std::vector<double> phi_rel;  // per iteration ||dphi||_2 / ||phi||_2
+    std::vector<double> error;                      // per iteration, max over ordinates of ||dpsi||_inf
+    std::vector<std::vector<double>> per_ordinate;  // error[it][d] (solver.hpp:36)
+    std::vector<double> phi_rel;                    // per iteration ||dphi||_2 / ||phi||_2
     bool converged = false;
     double seconds = 0.0;         // device time
     int iterations() const { return static_cast<int>(error.size()); }
@@ -86,8 +88,12 @@ class SweepSolver {
     // descriptor carries the mesh, basis order, ordinates, cross sections and
     // source (see hosweep_b200.h); options.weighting / exact_fas_threshold
     // override the descriptor's graph knobs.
+    // The reference constructor factors every local block and throws SolverError
+    // for a singular one (solver.hpp:67-75); check_local_blocks is therefore forced
+    // on here (one sweep on zero data at construction).
     explicit SweepSolver(hsw_problem_desc desc, const SolveOptions& opts = {}) : opts_(opts) {
         desc.abi_version = HSW_ABI_VERSION;
+        desc.check_local_blocks = 1;
         desc.weighting = static_cast<int>(opts.weighting);
         desc.exact_fas_threshold = opts.exact_fas_threshold;
         hsw_handle* h = nullptr;
@@ -99,6 +105,7 @@ class SweepSolver {
         nb_ = (int)sz[1];
         nd_ = (int)sz[2];
         orderings_.resize(nd_);
+        ordering_once_ = std::make_unique<std::once_flag[]>(nd_);
     }
 
     const SolveOptions& options() const { return opts_; }
@@ -111,7 +118,9 @@ class SweepSolver {
     const SweepOrdering& ordering(int d) const {
         if (d < 0 || d >= nd_) throw std::out_of_range("SweepSolver::ordering: ordinate " + std::to_string(d));
         auto& slot = orderings_[d];
-        if (!slot) {
+        // filled once per ordinate; safe under concurrent callers (the reference's
+        // orderings_ are built in the constructor and only read afterwards)
+        std::call_once(ordering_once_[d], [&] {
             auto o = std::make_unique<SweepOrdering>();
             o->order.resize(nel_);
             o->position.resize(nel_);
@@ -122,7 +131,7 @@ class SweepSolver {
             o->lagged_edges.resize(nl);
             check(hsw_ordering(h_.get(), d, nullptr, nullptr, o->lagged_edges.data(), nl, nullptr, nullptr, nullptr));
             slot = std::move(o);
-        }
+        });
         return *slot;
     }
 
@@ -162,7 +171,8 @@ class SweepSolver {
         hsw_si_result r{};
         const size_t N = (size_t)num_dofs();
         std::vector<double> psi(N * nd_), phi(N), err(opts_.max_iterations), rel(opts_.max_iterations);
-        check(hsw_source_iteration(h_.get(), &o, &r, psi.data(), phi.data(), err.data(), rel.data()));
+        std::vector<double> per((size_t)opts_.max_iterations * nd_);
+        check(hsw_source_iteration(h_.get(), &o, &r, psi.data(), phi.data(), err.data(), rel.data(), per.data()));
         SolverState s;
         s.psi.resize(nd_);
         for (int d = 0; d < nd_; ++d) s.psi[d].assign(psi.begin() + d * N, psi.begin() + (d + 1) * N);
@@ -171,6 +181,8 @@ class SweepSolver {
         ConvergenceHistory hst;
         hst.error.assign(err.begin(), err.begin() + r.iterations);
         hst.phi_rel.assign(rel.begin(), rel.begin() + r.iterations);
+        for (int it = 0; it < r.iterations; ++it)
+            hst.per_ordinate.emplace_back(per.begin() + (size_t)it * nd_, per.begin() + (size_t)(it + 1) * nd_);
         hst.converged = r.converged != 0;
         hst.seconds = r.seconds;
         return {std::move(s), std::move(hst)};
@@ -184,6 +196,7 @@ class SweepSolver {
     SolveOptions opts_;
     int nel_ = 0, nb_ = 0, nd_ = 0;
     mutable std::vector<std::unique_ptr<SweepOrdering>> orderings_;
+    std::unique_ptr<std::once_flag[]> ordering_once_;
 };
 
 }  // namespace hosweep_b200

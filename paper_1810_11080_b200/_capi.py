@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libhosweep_b200.so")
 
-HSW_ABI_VERSION = 1
+HSW_ABI_VERSION = 2
 HSW_OK = 0
 STATUS_NAMES = {
     -1: "HSW_ERR_INVALID", -2: "HSW_ERR_MESH", -3: "HSW_ERR_GEOMETRY", -4: "HSW_ERR_ASSEMBLY",
@@ -30,6 +30,7 @@ EXPORTED = [
     "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
     "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_sweep_host", "hsw_shard_phi_partial", "hsw_shard_psi_error",
     "hsw_shard_phi_norms", "hsw_shard_advance", "hsw_shard_psi", "hsw_debug_graph_order",
+    "hsw_debug_create_zero_block",
 ]
 
 
@@ -83,7 +84,7 @@ def load():
     L.hsw_sweep.argtypes = [vp, C.c_int, vp, vp, vp]
     L.hsw_sweep_device.argtypes = [vp, C.c_int, vp, vp, vp]
     L.hsw_direct_oracle.argtypes = [vp, C.c_int, vp, vp]
-    L.hsw_source_iteration.argtypes = [vp, C.POINTER(hsw_si_options), C.POINTER(hsw_si_result), vp, vp, vp, vp]
+    L.hsw_source_iteration.argtypes = [vp, C.POINTER(hsw_si_options), C.POINTER(hsw_si_result), vp, vp, vp, vp, vp]
     L.hsw_balance.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, vp]
     L.hsw_device_state.argtypes = [vp, vp, vp, vp]
     L.hsw_sweep_resident.argtypes = [vp]
@@ -95,6 +96,7 @@ def load():
     L.hsw_last_sweep_kernel_ms.argtypes = [vp]
     L.hsw_last_sweep_kernel_ms.restype = C.c_double
     L.hsw_debug_zero_block.argtypes = [vp, C.c_int, C.c_int]
+    L.hsw_debug_create_zero_block.argtypes = [C.c_int, C.c_int]
     L.hsw_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.hsw_debug_flags.argtypes = [vp, C.c_int]
     L.hsw_set_state.argtypes = [vp, vp, vp]

@@ -596,12 +596,15 @@ static void launch_dmma(const DevProblem& pr, const double* src, const double* p
                         double* psi_out, int64_t stride, const int* pairs, int npairs, const double* rhs_given,
                         unsigned long long* err, int64_t zero_pair, cudaStream_t st) {
     using G = DG<DIM, P, W>;
-    static bool configured = false;
-    if (!configured) {
+    static int slots[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    DCHECK(cudaGetDevice(&dev));
+    per_device_once(slots, mu, dev, [&] {
         DCHECK(cudaFuncSetAttribute(dmma_sweep_kernel<DIM, P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)G::SMEM));
-        configured = true;
-    }
+        return 1;
+    });
     const int blocks = (npairs + G::GROUPS - 1) / G::GROUPS;
     dmma_sweep_kernel<DIM, P, W><<<blocks, G::THREADS, G::SMEM, st>>>(pr, src, psi_old, psi_new_in, psi_out, stride,
                                                                       pairs, npairs, rhs_given, err, zero_pair);

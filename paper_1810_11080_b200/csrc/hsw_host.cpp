@@ -1316,6 +1316,10 @@ struct Setup {
 using namespace hsw;
 
 struct hsw_handle {
+    // calls on one handle are serialised (the reference's const sweep/local_solve are
+    // called concurrently for distinct ordinates, solver.hpp:145-149) and run on the
+    // handle's device whatever device is current on the calling thread
+    std::recursive_mutex mu;
     Setup S;
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -1374,6 +1378,21 @@ struct hsw_handle {
 
 namespace {
 thread_local std::string g_last_error;
+thread_local int g_create_zero_e = -1, g_create_zero_d = -1;
+
+// Lock the handle and make its device current for the call (restored on exit).
+struct HandleScope {
+    std::unique_lock<std::recursive_mutex> lk;
+    int prev = -1;
+    bool switched = false;
+    explicit HandleScope(hsw_handle* h) : lk(h->mu) {
+        if (h->stream && cudaGetDevice(&prev) == cudaSuccess && prev != h->device)
+            switched = cudaSetDevice(h->device) == cudaSuccess;
+    }
+    ~HandleScope() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
 
 int fail(int status, const std::string& msg) {
     g_last_error = msg;
@@ -1455,40 +1474,22 @@ void check_err(hsw_handle* h) {
     }
 }
 
-// Kernel selection (HSW_KERNEL): "dmma1" (one warp per pair, persistent,
-// hsw_dmma1.cu), "dmma" (W warps per pair, hsw_dmma.cu), "gj" (register-resident
-// DFMA Gauss-Jordan, hsw_gj.cu) or "v0" (simple SMEM LU, hsw_kernels.cu).
-// Unset / "auto" picks the fastest measured kernel per shape.
-int kernel_choice_env() {
-    static const int kc = [] {
-        const char* k = std::getenv("HSW_KERNEL");
-        if (k && std::string(k) == "v0") return 0;
-        if (k && std::string(k) == "gj") return 1;
-        if (k && std::string(k) == "dmma") return 2;
-        if (k && std::string(k) == "dmma1") return 3;
-        return -1;
-    }();
-    return kc;
-}
+// Kernel selection: the one-warp DMMA kernel (hsw_dmma1.cu) for every shape it
+// instantiates (2D Q2/Q3, 3D Q2-Q4: all five configs); the W-warps-per-pair DMMA
+// kernel (hsw_dmma.cu) for the other orders.  HSW_KERNEL=dmma forces the latter.
 int kernel_choice_for(int dim, int p) {
-    int env = kernel_choice_env();
-    if (env == 3 && !dev_dmma1_supported(dim, p)) env = -1;
-    if (env >= 0) return env;
-    if ((dim == 3 || dim == 2) && (p == 2 || p == 3)) return 3;   // one-warp DMMA (measured fastest)
-    if (dim == 3 && p == 4) return 3;                              // C5: dmma1 2.09 s vs gj 2.20 s per sweep
-    return (dim == 3 && p >= 2) ? 1 : 2;
+    static const bool force_dmma = [] {
+        const char* k = std::getenv("HSW_KERNEL");
+        return k && std::string(k) == "dmma";
+    }();
+    return (!force_dmma && dev_dmma1_supported(dim, p)) ? 3 : 2;
 }
-thread_local int g_kernel_dim = 2, g_kernel_p = 1;
-int kernel_choice() { return kernel_choice_for(g_kernel_dim, g_kernel_p); }
-bool use_v0() { return kernel_choice() == 0; }
 
 void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
-    switch (kernel_choice_for(h->S.dim, h->S.p)) {
-        case 0: dev_sweep_pairs(h->P, h->d_src, psi_old, psi_new, pairs, n, h->d_err, h->zero_pair, h->stream); break;
-        case 1: dev_gj_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream); break;
-        case 3: dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream); break;
-        default: dev_dmma_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
-    }
+    if (kernel_choice_for(h->S.dim, h->S.p) == 3)
+        dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+    else
+        dev_dmma_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
 }
 
 // All-ordinate sweep psi_old -> psi_new using the current h->d_src.
@@ -1693,6 +1694,45 @@ int guarded(F&& f) {
 }
 }  // namespace
 
+namespace {
+// SweepSolver::direct_oracle (solver.hpp:121-133) on the device: the per-ordinate
+// global system (block lower-triangular in the sweep order plus the lagged
+// couplings) is solved by lagged sweeps iterated to their fixed point,
+// x_{k+1} = sweep_d(phi, psi_old = x_k), from x_0 = it (device, N doubles; used as
+// scratch).  Converged when max|x_{k+1} - x_k| <= 16 eps max|x_{k+1}|, or at the
+// round-off floor (no decrease for 8 sweeps while <= 1e-11 max|x|); otherwise
+// HSW_ERR_SOLVER, like the reference's failed SparseLU (solver.hpp:130-131,190-192).
+// The result is left in res (device, N doubles).  Uses the current h->d_src.
+void direct_fixpoint(hsw_handle* h, int d, double* it, double* res) {
+    const size_t N = h->N;
+    const ptrdiff_t sh = (ptrdiff_t)d * (ptrdiff_t)N;
+    const bool exact_in_one = h->S.ords[d].lagged_edges.empty();
+    double best = INFINITY, diff = INFINITY, xmax = 0.0;
+    int since_best = 0;
+    constexpr int kMaxSweeps = 2000;
+    for (int k = 0; k < kMaxSweeps; ++k) {
+        run_dir_levels(h, d, it - sh, res - sh);
+        dev_max_abs_diff(res, it, (int64_t)N, h->d_scratch, h->d_out, h->stream);
+        CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaMemcpyAsync(it, res, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        check_err(h);   // synchronises
+        diff = h->h_out[0];
+        xmax = h->h_out[2];
+        if (exact_in_one || diff <= 16.0 * std::numeric_limits<double>::epsilon() * xmax) return;
+        if (diff < best) {
+            best = diff;
+            since_best = 0;
+        } else if (++since_best >= 8 && best <= 1e-11 * xmax) {
+            return;
+        }
+    }
+    char msg[160];
+    std::snprintf(msg, sizeof(msg), "direct oracle: lagged fixed point did not converge for ordinate %d "
+                  "(max |dpsi| = %.3e, max |psi| = %.3e)", d, diff, xmax);
+    throw hsw::Error(HSW_ERR_SOLVER, msg);
+}
+}  // namespace
+
 extern "C" {
 
 int hsw_last_error(char* buf, size_t len) {
@@ -1797,7 +1837,6 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             for (int a = 0; a < S.nfn; ++a) ct.fnode[f][a] = S.fnodes[f][a];
         for (int q = 0; q < S.nqf; ++q)
             for (int a = 0; a < S.nfn; ++a) ct.trace[q][a] = S.trace[(size_t)q * S.nfn + a];
-        dev_upload_tables(ct);
         {
             std::vector<int> fidx((size_t)kMaxFaces * 128, -1);
             for (int f = 0; f < S.nf; ++f)
@@ -1805,7 +1844,6 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             std::vector<double> line(64, 0.0);
             for (int i = 0; i < S.face_pts && i < 8; ++i)
                 for (int a = 0; a <= S.p && a < 8; ++a) line[(size_t)i * 8 + a] = S.basis.value(a, S.line_f.x[i]);
-            dev_upload_gj_tables(ct, fidx.data(), line.data());
             std::vector<int> fn((size_t)kMaxFaces * kMaxFaceNodes, 0), nmask(128, 0);
             std::vector<double> tr((size_t)kMaxFacePoints * kMaxFaceNodes, 0.0);
             for (int f = 0; f < kMaxFaces; ++f)
@@ -1898,6 +1936,10 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         P.g_fnode = h->d_tab_fnode; P.g_trace = h->d_tab_trace; P.g_fidx = h->d_tab_fidx;
         P.g_nmask = h->d_tab_nmask; P.g_line = h->d_tab_line;
         P.prof = h->d_prof;
+        // test hook (hsw_debug_create_zero_block): the (e, d) block zeroed from creation on
+        if (g_create_zero_e >= 0 && g_create_zero_e < S.nel && g_create_zero_d < S.nd)
+            h->zero_pair = (int64_t)g_create_zero_e * S.nd + g_create_zero_d;
+        g_create_zero_e = g_create_zero_d = -1;
         if (desc->check_local_blocks) {
             // SweepSolver ctor factor check (solver.hpp:67-75): one sweep on zero data
             dev_scatter_source(P, h->d_phi, h->d_src, h->stream);
@@ -1983,25 +2025,18 @@ int hsw_interior_faces(const hsw_handle* h, int* ints5, int cap, int* count) {
 int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out) {
     return guarded([&] {
         if (!h || !rhs || !out) throw hsw::Error(HSW_ERR_INVALID, "hsw_local_solve: null argument");
+        HandleScope hs(h);
         need_device(h);
         if (e < 0 || e >= h->S.nel || d < 0 || d >= h->S.nd)
             throw hsw::Error(HSW_ERR_RANGE, "hsw_local_solve: element/ordinate out of range");
         const size_t nb = h->S.nb;
         CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        g_kernel_dim = h->S.dim;
-        g_kernel_p = h->S.p;
-        if (use_v0()) {
-            dev_local_solve(h->P, e, d, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
-        } else {
-            const int pr = e * h->S.nd + d;
-            CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-            if (kernel_choice() == 1)
-                dev_gj_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
-            else if (kernel_choice() == 3)
-                dev_dmma1_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
-            else
-                dev_dmma_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
-        }
+        const int pr = e * h->S.nd + d;
+        CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+        if (kernel_choice_for(h->S.dim, h->S.p) == 3)
+            dev_dmma1_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        else
+            dev_dmma_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
         CUDA_OK(cudaMemcpyAsync(out, h->d_vec2, nb * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         check_err(h);
         return HSW_OK;
@@ -2011,6 +2046,7 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
 int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* psi_old_dev, double* psi_new_dev) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep_device: null handle");
+        HandleScope hs(h);
         need_device(h);
         if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
         dev_scatter_source(h->P, phi_dev, h->d_src, h->stream);
@@ -2043,6 +2079,7 @@ static void pipelined_range_sweep(hsw_handle* h, int r0, int r1, const double* p
             run_all_levels(h, h->d_psiA, h->d_psiB, false);
         else
             run_range_levels(h, range_list(h, r0, r1), h->d_psiA, h->d_psiB);
+        h->last_launches += 1;   // the scatter-source kernel
         CUDA_OK(cudaMemcpyAsync(psi_new, h->d_psiB + (size_t)r0 * N, N * nr * sizeof(double), cudaMemcpyDeviceToHost,
                                 h->stream));
         return;
@@ -2059,22 +2096,26 @@ static void pipelined_range_sweep(hsw_handle* h, int r0, int r1, const double* p
         CUDA_OK(cudaMemcpyAsync(h->d_psiA + off, psi_old + hoff, cnt, cudaMemcpyHostToDevice, h->copy_in));
         CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
     }
+    int64_t launches = 1;   // the scatter-source kernel
     for (int b = 0; b < nblk; ++b) {
         const int d0 = r0 + e2e_block_start(b, nblk, nr), d1 = r0 + e2e_block_start(b + 1, nblk, nr);
         const size_t off = (size_t)d0 * N, hoff = (size_t)(d0 - r0) * N, cnt = (size_t)(d1 - d0) * N * sizeof(double);
         CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
         run_range_levels(h, range_list(h, d0, d1), h->d_psiA, h->d_psiB);
+        launches += h->last_launches;
         CUDA_OK(cudaEventRecord(h->ev_sw[b], h->stream));
         CUDA_OK(cudaStreamWaitEvent(h->copy_out, h->ev_sw[b], 0));
         CUDA_OK(cudaMemcpyAsync(psi_new + hoff, h->d_psiB + off, cnt, cudaMemcpyDeviceToHost, h->copy_out));
     }
     CUDA_OK(cudaEventRecord(h->ev_cp[1], h->copy_out));
     CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_cp[1], 0));
+    h->last_launches = launches;   // summed over the sub-blocks
 }
 
 int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, double* psi_new) {
     return guarded([&] {
         if (!h || !phi || !psi_old || !psi_new) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep: null argument");
+        HandleScope hs(h);
         need_device(h);
         if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
         const size_t N = h->N;
@@ -2097,35 +2138,25 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
 int hsw_direct_oracle(hsw_handle* h, int d, const double* phi, double* psi) {
     return guarded([&] {
         if (!h || !phi || !psi) throw hsw::Error(HSW_ERR_INVALID, "hsw_direct_oracle: null argument");
+        HandleScope hs(h);
         need_device(h);
         if (d < 0 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_direct_oracle: ordinate out of range");
         const size_t N = h->N;
-        double* slotA = h->d_psiA + (size_t)d * N;
-        double* slotB = h->d_psiB + (size_t)d * N;
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-        CUDA_OK(cudaMemsetAsync(slotA, 0, N * sizeof(double), h->stream));
+        CUDA_OK(cudaMemsetAsync(h->d_vec, 0, N * sizeof(double), h->stream));
         dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
-        double prev = INFINITY;
-        for (int it = 0; it < 2000; ++it) {
-            run_dir_levels(h, d, h->d_psiA, h->d_psiB);
-            dev_max_abs_diff(slotA, slotB, (int64_t)N, h->d_scratch, h->d_out, h->stream);
-            CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-            CUDA_OK(cudaMemcpyAsync(slotA, slotB, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-            check_err(h);
-            const double diff = h->h_out[0];
-            if (h->S.ords[d].lagged_edges.empty() || diff == 0.0 || (diff >= prev && it > 3)) break;
-            prev = diff;
-        }
-        CUDA_OK(cudaMemcpyAsync(psi, slotB, N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        direct_fixpoint(h, d, h->d_vec, h->d_psiB + (size_t)d * N);
+        CUDA_OK(cudaMemcpyAsync(psi, h->d_psiB + (size_t)d * N, N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return HSW_OK;
     });
 }
 
 int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_result* res, double* psi_out,
-                         double* phi_out, double* err_hist, double* phi_hist) {
+                         double* phi_out, double* err_hist, double* phi_hist, double* per_ordinate_hist) {
     return guarded([&] {
         if (!h || !opts) throw hsw::Error(HSW_ERR_INVALID, "hsw_source_iteration: null argument");
+        HandleScope hs(h);
         need_device(h);
         const size_t N = h->N;
         const int nd = h->S.nd;
@@ -2143,26 +2174,22 @@ int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_resul
         for (int it = 0; it < opts->max_iterations; ++it) {
             dev_scatter_source(h->P, phi_cur, h->d_src, h->stream);
             if (opts->mode == HSW_MODE_DIRECT) {
-                // direct_oracle per ordinate with phi fixed (solver.hpp:145-149)
+                // direct_oracle per ordinate with phi fixed (solver.hpp:145-149), from psi_old
                 for (int d = 0; d < nd; ++d) {
-                    double* a = cur + (size_t)d * N;
-                    double* b = nxt + (size_t)d * N;
-                    CUDA_OK(cudaMemcpyAsync(h->d_vec, a, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-                    for (int k = 0; k < 2000; ++k) {
-                        // iterate on slot d of cur using a scratch copy so cur keeps psi_old
-                        run_dir_levels(h, d, h->d_vec - (ptrdiff_t)d * (ptrdiff_t)N, nxt);
-                        dev_max_abs_diff(h->d_vec, b, (int64_t)N, h->d_scratch, h->d_out, h->stream);
-                        CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-                        CUDA_OK(cudaMemcpyAsync(h->d_vec, b, N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-                        CUDA_OK(cudaStreamSynchronize(h->stream));
-                        if (h->S.ords[d].lagged_edges.empty() || h->h_out[0] == 0.0 || k > 200) break;
-                    }
+                    CUDA_OK(cudaMemcpyAsync(h->d_vec, cur + (size_t)d * N, N * sizeof(double), cudaMemcpyDeviceToDevice,
+                                            h->stream));
+                    direct_fixpoint(h, d, h->d_vec, nxt + (size_t)d * N);
                 }
             } else {
                 run_all_levels(h, cur, nxt, false);
             }
             dev_phi_and_norms(h->P, nxt, cur, phi_cur, phi_nxt, h->d_scratch, h->d_out, h->stream);
             CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            if (per_ordinate_hist) {
+                dev_per_ordinate_maxdiff(nxt, cur, nd, (int64_t)N, h->d_vec2, h->stream);
+                CUDA_OK(cudaMemcpyAsync(per_ordinate_hist + (size_t)it * nd, h->d_vec2, (size_t)nd * sizeof(double),
+                                        cudaMemcpyDeviceToHost, h->stream));
+            }
             check_err(h);
             const double err = h->h_out[0];
             const double num = h->h_out[1], den = h->h_out[2];
@@ -2202,6 +2229,7 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
                 int cap, int* count) {
     return guarded([&] {
         if (!h || !psi || !phi || !out5) throw hsw::Error(HSW_ERR_INVALID, "hsw_balance: null argument");
+        HandleScope hs(h);
         const Setup& S = h->S;
         const size_t N = h->N;
         const int nfn = S.nfn, nqf = S.nqf, nb = S.nb;
@@ -2281,6 +2309,7 @@ int hsw_device_state(hsw_handle* h, double** psi_a, double** psi_b, double** phi
 int hsw_set_state(hsw_handle* h, const double* phi, const double* psi) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_set_state: null handle");
+        HandleScope hs(h);
         need_device(h);
         if (phi) CUDA_OK(cudaMemcpyAsync(h->d_phi, phi, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         if (psi)
@@ -2294,6 +2323,7 @@ int hsw_set_state(hsw_handle* h, const double* phi, const double* psi) {
 int hsw_sweep_resident(hsw_handle* h) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_sweep_resident: null handle");
+        HandleScope hs(h);
         need_device(h);
         dev_scatter_source(h->P, h->d_phi, h->d_src, h->stream);
         run_all_levels(h, h->d_psiA, h->d_psiB, true);
@@ -2314,6 +2344,7 @@ void check_block(const hsw_handle* h, int d0, int d1, const char* what) {
 int hsw_shard_reset(hsw_handle* h) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_reset: null handle");
+        HandleScope hs(h);
         need_device(h);
         const size_t N = h->N, nd = (size_t)h->S.nd;
         CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
@@ -2326,11 +2357,11 @@ int hsw_shard_reset(hsw_handle* h) {
 int hsw_shard_sweep_host(hsw_handle* h, int d0, int d1, const double* phi, const double* psi_old, double* psi_new) {
     return guarded([&] {
         if (!h || !phi || !psi_old || !psi_new) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_sweep_host: null argument");
+        HandleScope hs(h);
         need_device(h);
         check_block(h, d0, d1, "hsw_shard_sweep_host");
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         pipelined_range_sweep(h, d0, d1, psi_old, psi_new);
-        h->last_launches += 1;
         check_err(h);
         return HSW_OK;
     });
@@ -2339,6 +2370,7 @@ int hsw_shard_sweep_host(hsw_handle* h, int d0, int d1, const double* phi, const
 int hsw_shard_sweep(hsw_handle* h, int d0, int d1, const double* phi_dev) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_sweep: null handle");
+        HandleScope hs(h);
         need_device(h);
         check_block(h, d0, d1, "hsw_shard_sweep");
         const auto& rl = range_list(h, d0, d1);
@@ -2352,6 +2384,7 @@ int hsw_shard_sweep(hsw_handle* h, int d0, int d1, const double* phi_dev) {
 int hsw_shard_phi_partial(hsw_handle* h, int d0, int d1, const double* prefix_dev, double* out_dev) {
     return guarded([&] {
         if (!h || !out_dev) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_phi_partial: null argument");
+        HandleScope hs(h);
         need_device(h);
         check_block(h, d0, d1, "hsw_shard_phi_partial");
         dev_phi_partial(h->P, h->d_psiB, d0, d1, prefix_dev, out_dev, h->stream);
@@ -2362,6 +2395,7 @@ int hsw_shard_phi_partial(hsw_handle* h, int d0, int d1, const double* prefix_de
 int hsw_shard_psi_error(hsw_handle* h, int d0, int d1, double* err) {
     return guarded([&] {
         if (!h || !err) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_psi_error: null argument");
+        HandleScope hs(h);
         need_device(h);
         check_block(h, d0, d1, "hsw_shard_psi_error");
         const size_t N = h->N;
@@ -2378,6 +2412,7 @@ int hsw_shard_phi_norms(hsw_handle* h, const double* phi_new_dev, const double* 
     return guarded([&] {
         if (!h || !phi_new_dev || !phi_old_dev || !out2)
             throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_phi_norms: null argument");
+        HandleScope hs(h);
         need_device(h);
         dev_phi_norms2(h->P, phi_new_dev, phi_old_dev, h->d_scratch, h->d_out, h->stream);
         CUDA_OK(cudaMemcpyAsync(h->h_out, h->d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -2391,6 +2426,7 @@ int hsw_shard_phi_norms(hsw_handle* h, const double* phi_new_dev, const double* 
 int hsw_shard_advance(hsw_handle* h, const double* phi_dev) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_advance: null handle");
+        HandleScope hs(h);
         need_device(h);
         std::swap(h->d_psiA, h->d_psiB);
         if (phi_dev)
@@ -2402,6 +2438,7 @@ int hsw_shard_advance(hsw_handle* h, const double* phi_dev) {
 int hsw_shard_psi(hsw_handle* h, int d0, int d1, double* psi) {
     return guarded([&] {
         if (!h || !psi) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_psi: null argument");
+        HandleScope hs(h);
         need_device(h);
         check_block(h, d0, d1, "hsw_shard_psi");
         const size_t N = h->N;
@@ -2415,6 +2452,7 @@ int hsw_shard_psi(hsw_handle* h, int d0, int d1, double* psi) {
 int hsw_synchronize(hsw_handle* h) {
     return guarded([&] {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_synchronize: null handle");
+        HandleScope hs(h);
         need_device(h);
         CUDA_OK(cudaStreamSynchronize(h->stream));
         check_err(h);
@@ -2482,6 +2520,13 @@ int hsw_debug_profile(hsw_handle* h, unsigned long long out[16]) {
     if (!h || !h->d_prof) return fail(HSW_ERR_INVALID, "hsw_debug_profile: no device state");
     cudaStreamSynchronize(h->stream);
     cudaMemcpy(out, h->d_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    return HSW_OK;
+}
+
+int hsw_debug_create_zero_block(int e, int d) {
+    if (e < 0 || d < 0) return fail(HSW_ERR_RANGE, "hsw_debug_create_zero_block: out of range");
+    g_create_zero_e = e;
+    g_create_zero_d = d;
     return HSW_OK;
 }
 

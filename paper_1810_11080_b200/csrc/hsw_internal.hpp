@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -15,6 +16,17 @@ struct Error : std::runtime_error {
     int status;
     Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
+
+// Per-device launch configuration of one kernel instantiation: the dynamic
+// shared-memory attribute is per device, so it is set (and the resident grid
+// size measured) once for every device a process launches on.  Thread-safe.
+template <typename Init>
+int per_device_once(int (&slots)[64], std::mutex& mu, int dev, Init&& init) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) throw std::runtime_error("device ordinal out of range");
+    if (slots[dev] == 0) slots[dev] = init();
+    return slots[dev];
+}
 
 constexpr int kMaxFaces = 6;
 constexpr int kMaxFaceNodes = 49;     // (p+1)^2 for p <= 6 (3D p <= 4 -> 25)
@@ -49,7 +61,7 @@ struct DevProblem {
     unsigned long long* prof; // [16] debug phase-cycle accumulators
 };
 
-// Host-computed tables that are uploaded to constant memory.
+// Host-computed reference-face tables (uploaded as the g_* global tables).
 struct SourceParams {
     double v[8];
 };
@@ -63,35 +75,21 @@ struct ConstTables {
 struct DevState;
 struct LaunchCounters { int64_t launches = 0; };
 
-void dev_upload_tables(const ConstTables& t);
 // scattering + volume source s[e][m] = qvol + (1/4pi) sigma_s M phi
 void dev_scatter_source(const DevProblem& P, const double* phi, double* src, void* stream);
-// one level of the sweep over an explicit pair list
-void dev_sweep_pairs(const DevProblem& P, const double* src, const double* psi_old, double* psi_new,
-                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair,
-                     void* stream);
 // phi = sum_d w_d psi[d] (d ascending), plus max|psi_new - psi_old| and the
 // phi L2 partial sums; deterministic fixed-shape reductions.
 void dev_phi_and_norms(const DevProblem& P, const double* psi_new, const double* psi_old,
                        const double* phi_old, double* phi_new, double* scratch, double* out3,
                        void* stream);
-// max_i |a_i - b_i| over n values
+// out[d] = max_i |a[d][i] - b[d][i]| for d < nd (per-ordinate error history)
+void dev_per_ordinate_maxdiff(const double* a, const double* b, int nd, int64_t n, double* out, void* stream);
+// out[0] = max_i |a_i - b_i|, out[2] = max_i |a_i| over n values
 void dev_max_abs_diff(const double* a, const double* b, int64_t n, double* scratch, double* out,
                       void* stream);
-// local solve A_{e,d} x = rhs for a single pair (test hook / API)
-void dev_local_solve(const DevProblem& P, int e, int d, const double* rhs, double* out,
-                     unsigned long long* err_key, int64_t zero_pair, void* stream);
-int dev_max_dynamic_smem_needed(int dim, int p);
 double dev_fp64_peak_tflops(int device);
 double dev_dmma_peak_tflops(int device);
-// production register-resident Gauss-Jordan sweep (hsw_gj.cu)
-void dev_upload_gj_tables(const ConstTables& t, const int* fidx /*6*128*/, const double* line /*8*8*/);
-void dev_gj_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
-                  const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
-void dev_gj_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
-                        unsigned long long* err_key, int64_t zero_pair, void* stream);
-int dev_gj_smem(int dim, int p);
-// production blocked Gauss-Jordan with DMMA trailing updates (hsw_dmma.cu)
+// W warps per pair, DMMA trailing updates (hsw_dmma.cu): the shapes dmma1 does not instantiate
 void dev_dmma_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream);
 void dev_dmma_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,

@@ -130,10 +130,15 @@ def _world(group) -> Tuple[int, int]:
     return 0, 1
 
 
-def sharded_source_iteration(backend, tolerance: float = 1e-8, max_iterations: int = 500,
-                             criterion: str = "phi_rel_l2", group=None, local_blocks: Optional[int] = None,
+def sharded_source_iteration(backend, tolerance: float = 1e-14, max_iterations: int = 400,
+                             criterion: str = "psi_linf", group=None, local_blocks: Optional[int] = None,
                              return_psi: bool = False) -> ShardedResult:
     """Source iteration with the ordinates sharded over the ranks of ``group``.
+
+    The stopping defaults are the reference's SolveOptions (solver.hpp:25-32:
+    tolerance 1e-14 on max_d ||dpsi_d||_inf, 400 iterations), the same as
+    ``SweepSolver.source_iteration``; pass ``tolerance=1e-8,
+    criterion="phi_rel_l2"`` for the configs' relative-phi criterion.
 
     ``local_blocks`` (single rank only) splits the ordinates into that many
     blocks handled in sequence by this process with the same chained phi: the

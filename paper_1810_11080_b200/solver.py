@@ -120,10 +120,12 @@ class SolverState:
 
 @dataclasses.dataclass
 class ConvergenceHistory:
-    error: List[float]
-    phi_rel: List[float]
+    """solver.hpp:34-39 (+ the configs' relative-phi history and the device time)."""
+    error: List[float]                 # per iteration, max over ordinates of ||dpsi_d||_inf
+    phi_rel: List[float]               # per iteration ||dphi||_2 / ||phi||_2
     converged: bool
     seconds: float = 0.0
+    per_ordinate: List[List[float]] = dataclasses.field(default_factory=list)   # error[it][d]
 
     def iterations(self) -> int:
         return len(self.error)
@@ -146,7 +148,7 @@ _WEIGHT = {"unity": 0, "face": 1, "siginvface": 2, "sig_inv_face": 2}
 
 class SweepSolver:
     def __init__(self, problem: Problem, options: Optional[SolveOptions] = None, device: int = 0,
-                 validate_geometry: bool = True, check_local_blocks: bool = False):
+                 validate_geometry: bool = True, check_local_blocks: bool = True):
         L = _capi.load()
         self.problem = problem
         self._options = options or SolveOptions()
@@ -182,6 +184,8 @@ class SweepSolver:
         d.weighting = _WEIGHT[self._options.weighting]
         d.exact_fas_threshold = self._options.exact_fas_threshold
         d.validate_geometry = int(validate_geometry)
+        # the reference constructor factors every local block and throws SolverError
+        # for a singular one (solver.hpp:67-75): on by default here too
         d.check_local_blocks = int(check_local_blocks)
         d.device = device  # < 0: host-only plan (graphs/orderings, no device state)
         h = C.c_void_p()
@@ -278,12 +282,20 @@ class SweepSolver:
         phi = np.zeros(self.num_dofs)
         eh = np.zeros(max(o.max_iterations, 1))
         ph = np.zeros(max(o.max_iterations, 1))
+        po = np.zeros((max(o.max_iterations, 1), self.num_ordinates))
         _check(_capi.load().hsw_source_iteration(self._h, C.byref(opts), C.byref(res), _p(psi), _p(phi),
-                                                 _p(eh), _p(ph)))
+                                                 _p(eh), _p(ph), _p(po)))
         it = res.iterations
         state = SolverState(psi, phi, it)
-        hist = ConvergenceHistory(list(eh[:it]), list(ph[:it]), bool(res.converged), res.seconds)
+        hist = ConvergenceHistory(list(eh[:it]), list(ph[:it]), bool(res.converged), res.seconds,
+                                  [list(r) for r in po[:it]])
         return state, hist
+
+    @staticmethod
+    def zero_block_at_create_for_test(e: int, d: int):
+        """test_solver.cpp:332-344 for the constructor: the next SweepSolver created on
+        this thread has the (e, d) local block zeroed from the start."""
+        _check(_capi.load().hsw_debug_create_zero_block(e, d))
 
     def zero_block_for_test(self, e: int, d: int):
         """test_solver.cpp:332-344 hook: the (e, d) local block is zeroed."""

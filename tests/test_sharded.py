@@ -137,6 +137,9 @@ def test_shard_sweep_host_matches_the_all_ordinate_sweep():
     phi = rng.uniform(0, 1, N)
     psi_old = rng.uniform(-0.5, 1.0, (nd, N))
     ref = s.sweep(-1, phi, psi_old)
+    # an independent path: per-ordinate sweeps (per-level launches, no sub-block pipeline)
+    for d in (0, 17, 39, 40, 63):
+        assert np.array_equal(s.sweep(d, phi, psi_old[d]), ref[d]), d
     for d0, d1 in ((0, nd), (16, 48), (40, 64)):
         blk_old = np.ascontiguousarray(psi_old[d0:d1])
         blk_new = np.empty_like(blk_old)
@@ -144,3 +147,5 @@ def test_shard_sweep_host_matches_the_all_ordinate_sweep():
                                     C.c_void_p(blk_new.ctypes.data))
         assert rc == 0, _capi.last_error()
         assert np.array_equal(blk_new, ref[d0:d1]), (d0, d1)
+        # launches summed over the pipelined sub-blocks: scatter + one dataflow launch each
+        assert L.hsw_last_launch_count(s.handle) >= 2
