@@ -1860,7 +1860,15 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             h->d_tab_line = dev_upload(line);
         }
         if (!S.T.empty()) {
-            h->d_T = dev_upload(S.T);
+            // host tensors are [E][n][m][4]; the device layout is planar (t_idx)
+            const int nb = S.nb;
+            std::vector<double> Tp(S.T.size());
+            for (size_t e = 0; e < (size_t)S.nel; ++e)
+                for (int n = 0; n < nb; ++n)
+                    for (int m = 0; m < nb; ++m)
+                        for (int k = 0; k < 4; ++k)
+                            Tp[hsw::t_idx(e, nb, m, n, k)] = S.T[((e * nb + n) * nb + m) * 4 + k];
+            h->d_T = dev_upload(Tp);
             h->d_qvol = dev_upload(S.qvol);
         } else {   // element tensors + source moments computed on the device (hsw_setup.cu)
             const size_t nb = (size_t)S.nb, nel = (size_t)S.nel;
@@ -1930,6 +1938,10 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         DevProblem& P = h->P;
         P.dim = S.dim; P.p = S.p; P.nb = S.nb; P.nfn = S.nfn; P.nqf = S.nqf; P.nfaces = S.nf;
         P.nel = S.nel; P.nd = S.nd;
+        {
+            const char* tv = std::getenv("HSW_TUNE");
+            P.tune = tv ? std::atoi(tv) : 0;
+        }
         P.T = h->d_T; P.sig_t = h->d_sig_t; P.bscale = h->d_bscale; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
         P.fgeom = h->d_fgeom; P.fnbr = h->d_fnbr; P.inflags = h->d_inflags;
         P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;

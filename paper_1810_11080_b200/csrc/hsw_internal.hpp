@@ -32,11 +32,25 @@ constexpr int kMaxFaces = 6;
 constexpr int kMaxFaceNodes = 49;     // (p+1)^2 for p <= 6 (3D p <= 4 -> 25)
 constexpr int kMaxFacePoints = 64;    // (p+2)^2 for p <= 6
 
+#ifdef __CUDACC__
+#define HSW_HD __host__ __device__
+#else
+#define HSW_HD
+#endif
+// Device layout of the element tensors T = (M, Gx, Gy, Gz), entry (row m, column n):
+// per (element, column) two planes of double2, (M, Gx) then (Gy, Gz), rows contiguous.
+// A warp loading rows 8 tr + g of columns 8 tc + 2 q + s (the DMMA fragment layout)
+// then reads whole 128-byte lines per plane (a [m][4] double4 layout fetched every
+// 32-byte sector twice through the two halves of its 256-bit load).
+HSW_HD inline size_t t_idx(size_t e, int nb, int m, int n, int k) {
+    return 2 * (((e * (size_t)nb + (size_t)n) * 2 + (size_t)(k >> 1)) * (size_t)nb + (size_t)m) + (size_t)(k & 1);
+}
+
 // Kernel-facing problem tables (device pointers), POD.
 struct DevProblem {
     int dim, p, nb, nfn, nqf, nfaces, nel, nd;
-    const double* T;          // [E][n][m][4] (column-major entry (m,n)): M, Gx, Gy, Gz
-                              // with G_k = -(d_k u)^T W u
+    const double* T;          // planar, see t_idx: [E][n][2][m][2] (column n, plane (M, Gx) | (Gy, Gz),
+                              // row m) with G_k = -(d_k u)^T W u
     const double* sig_t;      // [E]
     const double* sig_s;      // [E]
     const double* bscale;     // [E] max_ij (sig_t |M| + |Gx| + |Gy| + |Gz|)_ij >= max |volume part of A(Omega)|:
@@ -59,6 +73,7 @@ struct DevProblem {
                               // 8 per-phase clock64 counters into prof[], 16/32 warp subsets (dmma1
                               // profiling instantiations only)
     unsigned long long* prof; // [16] debug phase-cycle accumulators
+    int tune;                 // development knobs (HSW_TUNE, bit flags; 0 = production defaults)
 };
 
 // Host-computed reference-face tables (uploaded as the g_* global tables).

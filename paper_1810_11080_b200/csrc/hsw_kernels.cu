@@ -27,10 +27,9 @@ __global__ void scatter_source_kernel(const DevProblem pr, const double* __restr
     const int nb = pr.nb;
     if (i >= (int64_t)pr.nel * nb) return;
     const int e = (int)(i / nb), m = (int)(i - (i / nb) * nb);
-    const double* Tm = pr.T + ((size_t)e * nb * nb + (size_t)m) * 4;  // entry (m, n) at (n*nb + m)
     const double* ph = phi + (size_t)e * nb;
     double s = 0.0;
-    for (int n = 0; n < nb; ++n) s += Tm[(size_t)n * nb * 4] * ph[n];
+    for (int n = 0; n < nb; ++n) s += pr.T[t_idx(e, nb, m, n, 0)] * ph[n];   // M[m][n]
     const double c4pi = 1.0 / (4.0 * 3.14159265358979323846);
     src[i] = pr.qvol[i] + c4pi * (pr.sig_s[e] * s);
 }

@@ -98,7 +98,6 @@ element_tensor_kernel(int nel, int nb, int npe, int nq, const double* __restrict
     }
     // 3. T in 4 x 4 (m, n) blocks per thread, all DIM + 1 components
     const int nbb = (nb + 3) / 4;
-    double* Te = T + (size_t)e * nb * nb * 4;
     for (int blk = threadIdx.x; blk < nbb * nbb; blk += kSetupThreads) {
         const int m0 = 4 * (blk / nbb), n0 = 4 * (blk % nbb);
         double acc[4][4][DIM + 1];
@@ -138,11 +137,10 @@ element_tensor_kernel(int nel, int nb, int npe, int nq, const double* __restrict
             for (int j = 0; j < 4; ++j) {
                 const int m = m0 + i, n = n0 + j;
                 if (m < nb && n < nb) {
-                    double* o = Te + ((size_t)n * nb + m) * 4;
-                    o[0] = acc[i][j][0];
+                    T[t_idx(e, nb, m, n, 0)] = acc[i][j][0];
 #pragma unroll
-                    for (int k = 1; k <= DIM; ++k) o[k] = -acc[i][j][k];
-                    if (DIM == 2) o[3] = 0.0;
+                    for (int k = 1; k <= DIM; ++k) T[t_idx(e, nb, m, n, k)] = -acc[i][j][k];
+                    if (DIM == 2) T[t_idx(e, nb, m, n, 3)] = 0.0;
                 }
             }
     }
@@ -156,9 +154,8 @@ absorption_kernel(int nel, int nb, const double* __restrict__ T, const double* _
     const int64_t total = (int64_t)nel * nb;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int e = (int)(i / nb), n = (int)(i % nb);
-        const double* col = T + ((size_t)e * nb * nb + (size_t)n * nb) * 4;   // column n: M[m][n], m = 0..nb-1
-        double cs = 0.0;
-        for (int m = 0; m < nb; ++m) cs += col[(size_t)m * 4];
+        double cs = 0.0;   // column n of M: M[m][n], m = 0..nb-1
+        for (int m = 0; m < nb; ++m) cs += T[t_idx(e, nb, m, n, 0)];
         s += (sig_t[e] - sig_s[e]) * cs * phi[i];
     }
     __shared__ double red[256];
@@ -179,11 +176,11 @@ __global__ void __launch_bounds__(kSetupThreads) block_scale_kernel(int nb, cons
     __shared__ double red[kSetupThreads];
     const int e = blockIdx.x;
     const double st = sig_t[e];
-    const double4* Te = reinterpret_cast<const double4*>(T) + (size_t)e * nb * nb;
     double m = 0.0;
     for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) {
-        const double4 t = Te[i];
-        m = fmax(m, st * fabs(t.x) + fabs(t.y) + fabs(t.z) + fabs(t.w));
+        const int col = i / nb, row = i - (i / nb) * nb;
+        m = fmax(m, st * fabs(T[t_idx(e, nb, row, col, 0)]) + fabs(T[t_idx(e, nb, row, col, 1)]) +
+                        fabs(T[t_idx(e, nb, row, col, 2)]) + fabs(T[t_idx(e, nb, row, col, 3)]));
     }
     red[threadIdx.x] = m;
     __syncthreads();

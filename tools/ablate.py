@@ -8,12 +8,14 @@ P = pb.config(name)
 s = pk.SweepSolver(P)
 L = _capi.load()
 L.hsw_debug_flags.argtypes = [C.c_void_p, C.c_int]
-for flags in ([0] if os.environ.get("QUICK") else [0, 1, 2, 4, 3, 5, 6, 7]):
+FL = os.environ.get("FLAGS")
+for flags in ([int(x) for x in FL.split(",")] if FL else [0] if os.environ.get("QUICK") else [0, 1, 2, 4, 3, 5, 6, 7]):
     L.hsw_debug_flags(s.handle, flags)
     for _ in range(2):
         L.hsw_sweep_resident(s.handle); L.hsw_synchronize(s.handle)
     ms = L.hsw_last_sweep_kernel_ms(s.handle)
-    print(f"{name} flags={flags} (1 no-faces, 2 no-elim, 4 no-T) sweep {ms:.2f} ms", flush=True)
+    print(f"{name} flags={flags} (1 no-faces, 2 no-elim, 4 no-T, 64 no-TMEM-gather, 256 prof-only) sweep {ms:.2f} ms", flush=True)
+if os.environ.get("ONLY_FLAGS"): sys.exit(0)
 
 # per-phase clock64 counters (flag 8), cycles per pair as seen by one lane of the pair
 import numpy as np
