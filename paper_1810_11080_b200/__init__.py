@@ -10,5 +10,6 @@ from .solver import (  # noqa: F401
     SolveOptions, SweepOrdering, SolverState, ConvergenceHistory, BalanceReport, SweepSolver,
     balance_report, SolverError, MeshError, GeometryError, AssemblyError, HswError,
 )
+from .mesh_io import read_mesh, write_mesh, mesh_from_json, mesh_to_json, problem_from_mesh  # noqa: F401
 
 __version__ = "0.1.0"

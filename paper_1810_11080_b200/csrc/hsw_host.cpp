@@ -577,19 +577,37 @@ static std::vector<std::vector<int>> tarjan_scc(int n, const std::vector<Edge>& 
 struct Fas { std::vector<int> order, lagged; double weight = 0.0; };
 struct Local { std::vector<int> verts; std::vector<std::array<int, 2>> e; std::vector<double> w; std::vector<int> parent; };
 
-static Local induce(int nv, const std::vector<Edge>& edges, const std::vector<int>& vs,
-                    std::vector<int>& scratch) {  // sweepgraph.hpp:156-170
+// induce (sweepgraph.hpp:156-170) without the scan over every edge of the graph per component (O(E) per SCC,
+// quadratic on twisted meshes with many cyclic components): the component's out-edges
+// from the CSR adjacency, sorted by edge id, give the same local edge list in the same
+// (ascending edge id) order, so FAS tie-breaks and `parent` are unchanged.
+struct OutCsr { std::vector<int> off, eid; };
+static OutCsr out_csr(int nv, const std::vector<Edge>& edges) {
+    OutCsr g;
+    g.off.assign(nv + 1, 0);
+    for (const auto& ed : edges) g.off[ed.from + 1]++;
+    for (int v = 0; v < nv; ++v) g.off[v + 1] += g.off[v];
+    g.eid.resize(edges.size());
+    std::vector<int> fill(g.off.begin(), g.off.end() - 1);
+    for (size_t k = 0; k < edges.size(); ++k) g.eid[fill[edges[k].from]++] = (int)k;   // ascending per vertex
+    return g;
+}
+static Local induce_csr(const OutCsr& g, const std::vector<Edge>& edges, const std::vector<int>& vs,
+                        std::vector<int>& scratch, std::vector<int>& ks) {
     Local lg;
     lg.verts = vs;
-    if ((int)scratch.size() != nv) scratch.assign(nv, -1);
+    if (scratch.size() != g.off.size() - 1) scratch.assign(g.off.size() - 1, -1);
     for (size_t i = 0; i < vs.size(); ++i) scratch[vs[i]] = (int)i;
-    for (size_t k = 0; k < edges.size(); ++k) {
+    ks.clear();
+    for (int v : vs)
+        for (int j = g.off[v]; j < g.off[v + 1]; ++j)
+            if (scratch[edges[g.eid[j]].to] >= 0) ks.push_back(g.eid[j]);
+    std::sort(ks.begin(), ks.end());
+    for (int k : ks) {
         const auto& ed = edges[k];
-        if (scratch[ed.from] >= 0 && scratch[ed.to] >= 0) {
-            lg.e.push_back({scratch[ed.from], scratch[ed.to]});
-            lg.w.push_back(ed.weight);
-            lg.parent.push_back((int)k);
-        }
+        lg.e.push_back({scratch[ed.from], scratch[ed.to]});
+        lg.w.push_back(ed.weight);
+        lg.parent.push_back(k);
     }
     for (int v : vs) scratch[v] = -1;
     return lg;
@@ -728,14 +746,20 @@ static Ordering sweep_ordering(int n, const std::vector<Edge>& edges, int thr) {
         if (cin[c] == 0) ready.push({sccs[c].front(), c});
     Ordering res;
     res.order.reserve(n);
-    std::vector<int> scratch;
+    std::vector<int> scratch, ks;
+    OutCsr g;
+    bool have_csr = false;
     while (!ready.empty()) {
         const int c = ready.top().second;
         ready.pop();
         if (sccs[c].size() == 1) {
             res.order.push_back(sccs[c].front());
         } else {
-            const Local lg = induce(n, edges, sccs[c], scratch);
+            if (!have_csr) {
+                g = out_csr(n, edges);
+                have_csr = true;
+            }
+            const Local lg = induce_csr(g, edges, sccs[c], scratch, ks);
             const Fas fas = (int)sccs[c].size() <= std::min(thr, 22) ? fas_exact(lg) : fas_heuristic(lg);
             res.order.insert(res.order.end(), fas.order.begin(), fas.order.end());
             res.lagged_edges.insert(res.lagged_edges.end(), fas.lagged.begin(), fas.lagged.end());
@@ -992,8 +1016,11 @@ struct Setup {
             if (bad.load() != std::numeric_limits<int>::max())
                 throw Error(HSW_ERR_MESH, "mesh: element " + std::to_string(bad.load()) + " has non-positive Jacobian");
             // mesh.hpp:346-365 trace agreement on a 5-point (5x5) lattice
-            std::vector<double> v((size_t)mesh.npe), vr((size_t)mesh.npe);
-            for (size_t i = 0; i < mesh.ifaces.size(); ++i) {
+            std::atomic<int64_t> badf{std::numeric_limits<int64_t>::max()};
+            parallel_for((int64_t)mesh.ifaces.size(), [&](int64_t i) {
+                thread_local std::vector<double> v, vr;
+                v.resize((size_t)mesh.npe);
+                vr.resize((size_t)mesh.npe);
                 const auto& F = mesh.ifaces[i];
                 const double tol = 1e-12 * mesh.diameter(F.el);
                 const int nt = dim == 3 ? 5 : 1;
@@ -1010,11 +1037,18 @@ struct Setup {
                         mesh.map_tab(F.er, vr.data(), xr);
                         double d2 = 0.0;
                         for (int a = 0; a < dim; ++a) d2 += (xl[a] - xr[a]) * (xl[a] - xr[a]);
-                        if (std::sqrt(d2) > tol)
-                            throw Error(HSW_ERR_MESH, "mesh: interior face " + std::to_string(i) +
-                                                          " traces disagree between elements " +
-                                                          std::to_string(F.el) + " and " + std::to_string(F.er));
+                        if (std::sqrt(d2) > tol) {   // the lowest failing face is reported
+                            int64_t cur = badf.load();
+                            while (i < cur && !badf.compare_exchange_weak(cur, i)) {}
+                            return;
+                        }
                     }
+            });
+            if (badf.load() != std::numeric_limits<int64_t>::max()) {
+                const auto& F = mesh.ifaces[(size_t)badf.load()];
+                throw Error(HSW_ERR_MESH, "mesh: interior face " + std::to_string(badf.load()) +
+                                              " traces disagree between elements " + std::to_string(F.el) +
+                                              " and " + std::to_string(F.er));
             }
         }
     }
@@ -1236,19 +1270,26 @@ struct Setup {
             Ordering& o = ords[d];
             auto& lg = lagged[d];
             lg.assign(cpl.size(), 0);
-            std::vector<std::vector<int>> incoming(nel);
+            std::vector<int> in_off((size_t)nel + 1, 0), in_c(cpl.size());   // incoming couplings, CSR
             for (size_t c = 0; c < cpl.size(); ++c) {
                 lg[c] = o.position[cpl[c].up] > o.position[cpl[c].down];
-                incoming[cpl[c].down].push_back((int)c);
+                in_off[(size_t)cpl[c].down + 1]++;
                 uint16_t& fl = inflags[(size_t)d * nel + cpl[c].down];
                 fl |= (uint16_t)(1u << (2 * cpl[c].down_face));
                 if (lg[c]) fl |= (uint16_t)(1u << (2 * cpl[c].down_face + 1));
             }
+            for (int e = 0; e < nel; ++e) in_off[(size_t)e + 1] += in_off[e];
+            {
+                std::vector<int> fill(in_off.begin(), in_off.end() - 1);
+                for (size_t c = 0; c < cpl.size(); ++c) in_c[fill[cpl[c].down]++] = (int)c;
+            }
             o.level.assign(nel, 0);
             for (int e : o.order) {
                 int lv = 0;
-                for (int c : incoming[e])
+                for (int j = in_off[e]; j < in_off[(size_t)e + 1]; ++j) {
+                    const int c = in_c[j];
                     if (!lg[c]) lv = std::max(lv, o.level[cpl[c].up] + 1);
+                }
                 o.level[e] = lv;
             }
         });
@@ -1374,6 +1415,10 @@ struct hsw_handle {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_sw;
     cudaEvent_t ev_cp[2] = {nullptr, nullptr};
+    // pageable caller buffers: pinned staging ring (2 in + 2 out chunks), one event per chunk
+    char* stage = nullptr;
+    size_t stage_chunk = 0;
+    cudaEvent_t ev_stage[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -1434,6 +1479,9 @@ void free_handle(hsw_handle* h) {
         if (e) cudaEventDestroy(e);
     if (h->copy_in) cudaStreamDestroy(h->copy_in);
     if (h->copy_out) cudaStreamDestroy(h->copy_out);
+    if (h->stage) cudaFreeHost(h->stage);
+    for (auto e : h->ev_stage)
+        if (e) cudaEventDestroy(e);
     if (h->h_out) cudaFreeHost(h->h_out);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -2079,9 +2127,133 @@ int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* 
 // block's sweep needs only its own psi_old (lagged couplings stay within an
 // ordinate), so the H2D of block b+1 and the D2H of block b-1 overlap the sweep of
 // block b.  Stream-ordered on h->stream (the caller synchronizes).
+// True for page-locked (cudaHostAlloc / cudaHostRegister) or managed host memory: the
+// copy engines read / write it asynchronously.  Ordinary pageable memory is not.
+static bool copy_engine_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// memcpy of one staging chunk split over the host workers (pageable caller memory is
+// first-touched here, so the page faults are spread over the cores as well)
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t piece = (size_t)4 << 20;
+    const int64_t np = (int64_t)((bytes + piece - 1) / piece);
+    parallel_for(np, [&](int64_t i) {
+        const size_t off = (size_t)i * piece, len = std::min(piece, bytes - off);
+        std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len);
+    });
+}
+
+// staging chunk (HSW_STAGE_MB overrides; 64 MiB default)
+static size_t stage_chunk_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("HSW_STAGE_MB");
+        const long mb = e ? std::atol(e) : 64;
+        return (size_t)std::max(1l, mb) << 20;
+    }();
+    return v;
+}
+
+// pipelined_range_sweep for PAGEABLE caller buffers (what a reference caller passes:
+// Eigen / std::vector / numpy storage).  The copy engines cannot stream pageable memory
+// asynchronously, so every transfer goes through a pinned staging ring: host workers
+// memcpy the next chunk of psi_old into an input stage while the previous stage's
+// H2D copy and the sweeps of earlier ordinate blocks run, and drain the D2H output
+// stages of finished blocks into psi_new.  Host order per block b: H2D(b), sweep(b),
+// then the D2H of block b-1, so the GPU always has the next sweep queued while the host
+// waits on a drain.  Synchronous on return (the caller's buffers are written).
+static void staged_range_sweep(hsw_handle* h, int r0, int r1, const double* psi_old, double* psi_new) {
+    const size_t N = h->N;
+    const int nr = r1 - r0;
+    const int nblk = std::max(2, e2e_blocks(h, nr));
+    ensure_copy_streams(h, nblk);
+    const size_t CH = stage_chunk_bytes();
+    if (!h->stage || h->stage_chunk != CH) {
+        if (h->stage) CUDA_OK(cudaFreeHost(h->stage));
+        h->stage = nullptr;
+        CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&h->stage), 4 * CH, cudaHostAllocDefault));
+        h->stage_chunk = CH;
+        for (auto& e : h->ev_stage)
+            if (!e) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    auto bstart = [&](int b) { return r0 + e2e_block_start(b, nblk, nr); };
+    for (int b = 0; b < nblk; ++b) (void)range_list(h, bstart(b), bstart(b + 1));
+    // inputs of the whole range are read after this point: order against earlier work
+    CUDA_OK(cudaEventRecord(h->ev_cp[0], h->stream));
+    CUDA_OK(cudaStreamWaitEvent(h->copy_in, h->ev_cp[0], 0));
+    dev_scatter_source(h->P, h->d_phi_old, h->d_src, h->stream);
+    int in_slot = 0;
+    bool in_used[2] = {false, false};
+    auto h2d = [&](int b) {
+        const size_t off = (size_t)bstart(b) * N * sizeof(double), end = (size_t)bstart(b + 1) * N * sizeof(double);
+        const size_t hbase = (size_t)r0 * N * sizeof(double);
+        for (size_t o = off; o < end; o += CH) {
+            const size_t len = std::min(CH, end - o);
+            char* st = h->stage + (size_t)in_slot * CH;
+            if (in_used[in_slot]) CUDA_OK(cudaEventSynchronize(h->ev_stage[in_slot]));   // its last copy is done
+            parallel_memcpy(st, reinterpret_cast<const char*>(psi_old) + (o - hbase), len);
+            CUDA_OK(cudaMemcpyAsync(reinterpret_cast<char*>(h->d_psiA) + o, st, len, cudaMemcpyHostToDevice,
+                                    h->copy_in));
+            CUDA_OK(cudaEventRecord(h->ev_stage[in_slot], h->copy_in));
+            in_used[in_slot] = true;
+            in_slot ^= 1;
+        }
+        CUDA_OK(cudaEventRecord(h->ev_in[b], h->copy_in));
+    };
+    int64_t launches = 1;   // the scatter-source kernel
+    auto sweep = [&](int b) {
+        CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
+        run_range_levels(h, range_list(h, bstart(b), bstart(b + 1)), h->d_psiA, h->d_psiB);
+        launches += h->last_launches;
+        CUDA_OK(cudaEventRecord(h->ev_sw[b], h->stream));
+    };
+    auto d2h = [&](int b) {
+        CUDA_OK(cudaStreamWaitEvent(h->copy_out, h->ev_sw[b], 0));
+        const size_t off = (size_t)bstart(b) * N * sizeof(double), end = (size_t)bstart(b + 1) * N * sizeof(double);
+        const size_t hbase = (size_t)r0 * N * sizeof(double);
+        // two output stages: the copy of chunk k+1 runs while chunk k is drained
+        std::vector<size_t> chunks;
+        for (size_t o = off; o < end; o += CH) chunks.push_back(o);
+        auto issue = [&](size_t k) {
+            const size_t o = chunks[k], len = std::min(CH, end - o);
+            char* st = h->stage + (2 + k % 2) * CH;
+            CUDA_OK(cudaMemcpyAsync(st, reinterpret_cast<const char*>(h->d_psiB) + o, len, cudaMemcpyDeviceToHost,
+                                    h->copy_out));
+            CUDA_OK(cudaEventRecord(h->ev_stage[2 + k % 2], h->copy_out));
+        };
+        if (!chunks.empty()) issue(0);
+        for (size_t k = 0; k < chunks.size(); ++k) {
+            CUDA_OK(cudaEventSynchronize(h->ev_stage[2 + k % 2]));
+            if (k + 1 < chunks.size()) issue(k + 1);
+            const size_t o = chunks[k], len = std::min(CH, end - o);
+            parallel_memcpy(reinterpret_cast<char*>(psi_new) + (o - hbase), h->stage + (2 + k % 2) * CH, len);
+        }
+    };
+    h2d(0);
+    sweep(0);
+    for (int b = 1; b < nblk; ++b) {
+        h2d(b);
+        sweep(b);
+        d2h(b - 1);
+    }
+    d2h(nblk - 1);
+    CUDA_OK(cudaEventRecord(h->ev_cp[1], h->copy_out));
+    CUDA_OK(cudaStreamWaitEvent(h->stream, h->ev_cp[1], 0));
+    h->last_launches = launches;
+}
+
 static void pipelined_range_sweep(hsw_handle* h, int r0, int r1, const double* psi_old, double* psi_new) {
     const size_t N = h->N;
     const int nr = r1 - r0;
+    if ((double)N * nr * sizeof(double) >= 64e6 && !(copy_engine_host(psi_old) && copy_engine_host(psi_new))) {
+        staged_range_sweep(h, r0, r1, psi_old, psi_new);
+        return;
+    }
     const int nblk = e2e_blocks(h, nr);
     if (nblk <= 1) {
         CUDA_OK(cudaMemcpyAsync(h->d_psiA + (size_t)r0 * N, psi_old, N * nr * sizeof(double), cudaMemcpyHostToDevice,

@@ -343,3 +343,32 @@ def test_concurrent_sweeps_from_cpp_threads(tmp_path):
     ref = O.OracleSolver(prob).sweep_all(phi, psi_old)
     for d in range(nd):
         assert rel_l2(got[d], ref[d]) <= SWEEP_TOL, d
+
+
+# ------------------------------------------------- host buffers: pageable vs pinned
+def test_pageable_host_sweep_equals_pinned_and_resident():
+    """hsw_sweep(d = -1) from PAGEABLE caller memory (numpy, what SweepSolver.sweep
+    passes; solver.hpp:98 callers hand Eigen storage) goes through the pinned staging
+    ring; from pinned memory through the copy-engine pipeline; the resident path is
+    one dataflow launch.  Same pairs, same inputs: bit-identical psi.  64 ordinates of
+    the C4 mesh (1.07 GB of psi: many staging chunks per ordinate block)."""
+    import torch
+    prob = pb.config("c4", n_mu=4, n_az=16)
+    s = pk.SweepSolver(prob)
+    nd, N = prob.num_ordinates, prob.num_dofs
+    rng = np.random.default_rng(3)
+    phi = rng.uniform(0.0, 1.0, N)
+    psi_old = rng.uniform(-0.5, 1.0, (nd, N))
+    got_pageable = s.sweep(-1, phi, psi_old)
+    L = _capi.load()
+    po = torch.from_numpy(psi_old).pin_memory()
+    pn = torch.empty((nd, N), dtype=torch.float64).pin_memory()
+    assert L.hsw_sweep(s.handle, -1, _p(phi), C.c_void_p(po.data_ptr()), C.c_void_p(pn.data_ptr())) == 0, \
+        _capi.last_error()
+    assert np.array_equal(got_pageable, pn.numpy())
+    _resident_sweep(s, phi, psi_old)
+    for d in (0, nd // 3, nd - 1):
+        assert np.array_equal(_extract(s, d), got_pageable[d]), d
+    # and one ordinate against the CPU oracle
+    orc = O.OracleSolver(prob, cache_lu=False, check_rcond=False, active=[nd // 3])
+    assert rel_l2(got_pageable[nd // 3], orc.sweep(nd // 3, phi, psi_old[nd // 3])) <= SWEEP_TOL
