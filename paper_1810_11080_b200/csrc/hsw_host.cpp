@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <sys/mman.h>
 #include <exception>
 #include <limits>
 #include <map>
@@ -2170,6 +2171,14 @@ static size_t stage_chunk_bytes() {
 static void staged_range_sweep(hsw_handle* h, int r0, int r1, const double* psi_old, double* psi_new) {
     const size_t N = h->N;
     const int nr = r1 - r0;
+    {
+        // the output is usually freshly allocated by the caller (the reference returns psi by
+        // value): ask for transparent huge pages so that first-touch faults come per 2 MiB,
+        // not per 4 KiB (a policy hint on the caller's mapping; ignored where THP is off)
+        const uintptr_t a = reinterpret_cast<uintptr_t>(psi_new), pg = 4096;
+        const uintptr_t lo = a & ~(pg - 1), hi = (a + (uintptr_t)nr * N * sizeof(double) + pg - 1) & ~(pg - 1);
+        (void)madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+    }
     const int nblk = std::max(2, e2e_blocks(h, nr));
     ensure_copy_streams(h, nblk);
     const size_t CH = stage_chunk_bytes();

@@ -259,10 +259,18 @@ class SweepSolver:
         _check(_capi.load().hsw_local_solve(self._h, e, d, _p(rhs), _p(out)))
         return out
 
-    def sweep(self, d: int, phi, psi_old) -> np.ndarray:
+    def sweep(self, d: int, phi, psi_old, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """solver.hpp:98-117.  d = -1 sweeps every ordinate (psi_old / the result are
+        (num_ordinates, num_dofs)).  ``out`` (optional, C-contiguous float64 of psi_old's
+        shape, not aliasing it) receives the result instead of a freshly allocated array:
+        a fresh multi-GB array pays the OS's first-touch page faults on every call."""
         phi = np.ascontiguousarray(phi, np.float64)
         psi_old = np.ascontiguousarray(psi_old, np.float64)
-        out = np.zeros_like(psi_old)
+        if out is None:
+            out = np.zeros_like(psi_old)
+        elif (out.dtype != np.float64 or out.shape != psi_old.shape or not out.flags.c_contiguous
+              or np.shares_memory(out, psi_old)):
+            raise ValueError("sweep: out must be a C-contiguous float64 array of psi_old's shape, not aliasing it")
         _check(_capi.load().hsw_sweep(self._h, d, _p(phi), _p(psi_old), _p(out)))
         return out
 
