@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HSW_ABI_VERSION 2
+#define HSW_ABI_VERSION 3
 
 enum hsw_status {
     HSW_OK = 0,
@@ -95,7 +95,16 @@ typedef struct hsw_problem_desc {
                                    the first singular one, like the SweepSolver ctor
                                    (solver.hpp:67-75)                                   */
     int device;                 /* CUDA device ordinal                                  */
+    /* FaceIntegration (assembly.hpp:33-40): HSW_FACE_GAUSS (face_points per axis) or
+       HSW_FACE_ROMBERG, the reference's default: adaptive Romberg per (face, ordinate)
+       with tol / max_levels / min_levels (romberg.hpp:33-88; 2D meshes, as the
+       reference).  Zero-initialised fields select Gauss.                              */
+    int face_rule;
+    double romberg_tol;         /* default 1e-10 when <= 0                               */
+    int romberg_max_levels;     /* default 16 when <= 0                                  */
+    int romberg_min_levels;     /* default 6 when < 0 (0 is a valid value)              */
 } hsw_problem_desc;
+enum hsw_face_rule { HSW_FACE_GAUSS = 0, HSW_FACE_ROMBERG = 1 };
 
 /* SolveOptions (solver.hpp:25-32) + the configs' relative-phi criterion. */
 enum hsw_criterion { HSW_CRIT_PSI_LINF = 0, HSW_CRIT_PHI_REL_L2 = 1 };

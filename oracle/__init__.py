@@ -38,6 +38,8 @@ class orc_problem(C.Structure):
         ("weighting", C.c_int), ("fas_threshold", C.c_int),
         ("validate_geometry", C.c_int), ("cache_lu", C.c_int), ("check_rcond", C.c_int),
         ("num_active", C.c_int), ("active", C.c_void_p),
+        ("face_rule", C.c_int), ("romberg_tol", C.c_double), ("romberg_max_levels", C.c_int),
+        ("romberg_min_levels", C.c_int),
     ]
 
 
@@ -131,6 +133,10 @@ class OracleSolver:
         s.inflow = prob.inflow
         s.volume_points, s.face_points = prob.volume_points, prob.face_points
         s.weighting, s.fas_threshold = prob.weighting, prob.fas_threshold
+        s.face_rule = int(getattr(prob, "face_rule", 0))
+        s.romberg_tol = float(getattr(prob, "romberg_tol", 1e-10))
+        s.romberg_max_levels = int(getattr(prob, "romberg_max_levels", 16))
+        s.romberg_min_levels = int(getattr(prob, "romberg_min_levels", 6))
         s.validate_geometry, s.cache_lu, s.check_rcond = int(validate), int(cache_lu), int(check_rcond)
         if active is not None:
             act = arr(active, np.int32)

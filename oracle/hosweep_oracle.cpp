@@ -59,6 +59,61 @@ namespace orc {
 struct MeshError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct GeometryError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct AssemblyError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IntegrationError : std::runtime_error { using std::runtime_error::runtime_error; };  // romberg.hpp:15-17
+
+// romberg.hpp:33-88: Romberg tableau over successive trapezoid halvings of [0,1] for a
+// vector integrand f(t, out[nv]) (all components share one sampling).  Converged when two
+// successive diagonal entries agree to tol in the max norm, not before min_levels
+// halvings; otherwise the last diagonal entry is returned unconverged.  Elementwise
+// arithmetic in the reference's order (Eigen expressions evaluate coefficient-wise).
+template <typename F>
+static bool romberg_vec(F&& f, size_t nv, double tol, int max_levels, int min_levels, std::vector<double>& out) {
+    if (tol <= 0.0) throw std::invalid_argument("romberg: tol must be positive");
+    if (max_levels < 1) throw std::invalid_argument("romberg: need max_levels >= 1");
+    min_levels = std::min(min_levels, max_levels);
+    auto nan_check = [&](const std::vector<double>& v) {
+        for (double x : v)
+            if (std::isnan(x)) throw IntegrationError("romberg: integrand returned NaN");
+    };
+    std::vector<double> f0(nv), f1(nv), trap(nv), sum(nv), fi(nv);
+    f(0.0, f0.data());
+    f(1.0, f1.data());
+    nan_check(f0);
+    nan_check(f1);
+    for (size_t i = 0; i < nv; ++i) trap[i] = 0.5 * (f0[i] + f1[i]);
+    std::vector<std::vector<double>> diag{trap}, row;
+    bool converged = false;
+    long n = 1;
+    for (int k = 1; k <= max_levels; ++k) {
+        const double h = 1.0 / (2.0 * n);
+        f(h, sum.data());
+        nan_check(sum);
+        for (long i = 1; i < n; ++i) {
+            f((2 * i + 1) * h, fi.data());
+            nan_check(fi);
+            for (size_t j = 0; j < nv; ++j) sum[j] += fi[j];
+        }
+        for (size_t j = 0; j < nv; ++j) trap[j] = 0.5 * trap[j] + h * sum[j];
+        n *= 2;
+        row.assign(1, trap);
+        double pow4 = 1.0;
+        for (int j = 1; j <= k; ++j) {
+            pow4 *= 4.0;
+            std::vector<double> r(nv);
+            for (size_t i = 0; i < nv; ++i) r[i] = row[j - 1][i] + (row[j - 1][i] - diag[j - 1][i]) / (pow4 - 1.0);
+            row.push_back(std::move(r));
+        }
+        double diff = 0.0;
+        for (size_t i = 0; i < nv; ++i) diff = std::max(diff, std::abs(row[k][i] - diag[k - 1][i]));
+        diag.swap(row);
+        if (diff < tol && k >= min_levels) {
+            converged = true;
+            break;
+        }
+    }
+    out = diag.back();
+    return converged;
+}
 struct SolverError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // ---------------------------------------------------------------- parallel.hpp
@@ -771,6 +826,10 @@ struct Problem {
     std::map<int, CrossSections> xs;
     SourceSpec source;
     int vol_points = 0, face_points = 0;
+    // FaceIntegration (assembly.hpp:33-40): 0 gauss (face_points), 1 romberg (2D, the reference default)
+    int face_rule = 0;
+    double romberg_tol = 1e-10;
+    int romberg_max_levels = 16, romberg_min_levels = 6;
     int weighting = 1;      // 0 unity, 1 face, 2 siginvface (sweepgraph.hpp:40)
     int fas_threshold = 10; // solver.hpp:31
 };
@@ -782,6 +841,7 @@ struct PerOrdinate {
     std::vector<std::vector<double>> bout;    // per boundary face, restricted outflow
     std::vector<double> src_bnd;              // N*nb
     std::vector<double> face_length;
+    int unconverged = 0;                      // Romberg faces that hit max_levels (assembly.hpp:349)
     // graph / ordering
     std::vector<int> order, position, lagged_edges;
     double lagged_weight = 0.0;
@@ -960,8 +1020,116 @@ class Oracle {
         (void)n1;
     }
 
+    // assembly.hpp:185-268 + 302-313 with FaceIntegration::Rule::romberg (:121-131, the
+    // reference default; 2D): per interior face ONE Romberg tableau over the packed
+    // integrand [LL+ | RR- | LR- | RL+ | |J|] (face-node restriction: the other entries
+    // are exact zeros in every sample, so the max-norm convergence test is unchanged);
+    // per boundary face one over [LL+] and one over the inflow moments.
+    void assemble_faces_romberg(int d, PerOrdinate& ord) const {
+        const Mesh& M = P.mesh;
+        if (M.dim != 2) throw std::invalid_argument("romberg face rule: 2D meshes only (the reference is 2D)");
+        const double* omega = P.quad[d].dir;
+        const int nfn = nf_nodes, nn = nfn * nfn;
+        const int nfi = (int)M.ifaces.size();
+        ord.ll.assign(nfi, {});
+        ord.rr.assign(nfi, {});
+        ord.face_length.assign(nfi, 0.0);
+        ord.couplings.clear();
+        ord.unconverged = 0;
+        std::vector<double> ul(nfn), ur(nfn), packed;
+        for (int fi = 0; fi < nfi; ++fi) {
+            const FaceRecord& fr = M.ifaces[fi];
+            auto integrand = [&](double t, double* v) {   // assembly.hpp:197-220
+                const FaceGeom fg = M.face_geometry(fr.elem_left, fr.face_left, t, 0.0);
+                const double on = omega[0] * fg.normal[0] + omega[1] * fg.normal[1];
+                face_trace(fr.face_left, t, 0.0, ul.data());
+                double so, to;
+                orient_param(2, fr.orientation, t, 0.0, so, to);
+                face_trace(fr.face_right, so, to, ur.data());
+                const double wplus = 0.5 * (on + std::abs(on));
+                const double wminus = 0.5 * (std::abs(on) - on);
+                int k = 0;
+                for (int m = 0; m < nfn; ++m)
+                    for (int n = 0; n < nfn; ++n) v[k++] = wplus * ul[m] * ul[n] * fg.sj;
+                for (int m = 0; m < nfn; ++m)
+                    for (int n = 0; n < nfn; ++n) v[k++] = wminus * ur[m] * ur[n] * fg.sj;
+                for (int m = 0; m < nfn; ++m)
+                    for (int n = 0; n < nfn; ++n) v[k++] = wminus * ul[m] * ur[n] * fg.sj;
+                for (int m = 0; m < nfn; ++m)
+                    for (int n = 0; n < nfn; ++n) v[k++] = wplus * ur[m] * ul[n] * fg.sj;
+                v[k] = fg.sj;
+            };
+            if (!romberg_vec(integrand, (size_t)4 * nn + 1, P.romberg_tol, P.romberg_max_levels,
+                             P.romberg_min_levels, packed))
+                ord.unconverged++;
+            const double length = packed[(size_t)4 * nn];
+            ord.face_length[fi] = length;
+            const double eps_edge = 1e-12 * length;
+            ord.ll[fi].assign(packed.begin(), packed.begin() + nn);
+            ord.rr[fi].assign(packed.begin() + nn, packed.begin() + 2 * nn);
+            std::vector<double> LR(packed.begin() + 2 * nn, packed.begin() + 3 * nn),
+                RL(packed.begin() + 3 * nn, packed.begin() + 4 * nn);
+            double mlr = 0.0, mrl = 0.0;
+            for (int k = 0; k < nn; ++k) {
+                mlr = std::max(mlr, std::abs(LR[k]));
+                mrl = std::max(mrl, std::abs(RL[k]));
+            }
+            if (mlr > eps_edge) {
+                Coupling c{fi, fr.elem_left, fr.elem_right, fr.face_left, fr.face_right, LR};
+                for (double& x : c.block) x = -x;
+                ord.couplings.push_back(std::move(c));
+            }
+            if (mrl > eps_edge) {
+                Coupling c{fi, fr.elem_right, fr.elem_left, fr.face_right, fr.face_left, RL};
+                for (double& x : c.block) x = -x;
+                ord.couplings.push_back(std::move(c));
+            }
+        }
+        const int nfb = (int)M.bfaces.size();
+        ord.bout.assign(nfb, {});
+        ord.src_bnd.assign((size_t)nel * nb, 0.0);
+        for (int bi = 0; bi < nfb; ++bi) {
+            const BoundaryFace& bf = M.bfaces[bi];
+            auto outflow = [&](double t, double* v) {   // assembly.hpp:244-258
+                const FaceGeom fg = M.face_geometry(bf.elem, bf.local_face, t, 0.0);
+                const double on = omega[0] * fg.normal[0] + omega[1] * fg.normal[1];
+                face_trace(bf.local_face, t, 0.0, ul.data());
+                const double wplus = 0.5 * (on + std::abs(on));
+                int k = 0;
+                for (int m = 0; m < nfn; ++m)
+                    for (int n = 0; n < nfn; ++n) v[k++] = wplus * ul[m] * ul[n] * fg.sj;
+            };
+            if (!romberg_vec(outflow, (size_t)nn, P.romberg_tol, P.romberg_max_levels, P.romberg_min_levels,
+                             ord.bout[bi]))
+                ord.unconverged++;
+        }
+        // assemble_source's boundary functional (assembly.hpp:302-313), after the volume part
+        for (int bi = 0; bi < nfb; ++bi) {
+            const BoundaryFace& bf = M.bfaces[bi];
+            auto incident = [&](double t, double* v) {
+                const FaceGeom fg = M.face_geometry(bf.elem, bf.local_face, t, 0.0);
+                const double on = omega[0] * fg.normal[0] + omega[1] * fg.normal[1];
+                face_trace(bf.local_face, t, 0.0, ul.data());
+                const double wminus = 0.5 * (std::abs(on) - on);
+                const double c = wminus * P.source.inflow * fg.sj;
+                for (int m = 0; m < nfn; ++m) v[m] = c * ul[m];
+            };
+            std::vector<double> mom;
+            romberg_vec(incident, (size_t)nfn, P.romberg_tol, P.romberg_max_levels, P.romberg_min_levels, mom);
+            const auto& fn = fnodes[bf.local_face];
+            for (int m = 0; m < nfn; ++m) ord.src_bnd[(size_t)bf.elem * nb + fn[m]] += mom[m];
+        }
+        ord.incoming.assign(nel, {});
+        for (size_t c = 0; c < ord.couplings.size(); ++c)
+            ord.incoming[ord.couplings[c].downwind].push_back((int)c);
+    }
+
     // assembly.hpp:185-268 with FaceIntegration::Rule::gauss (:121-128)
     void assemble_faces(int d, PerOrdinate& ord) const {
+        if (P.face_rule == 1) {
+            assemble_faces_romberg(d, ord);
+            return;
+        }
         const Mesh& M = P.mesh;
         const int dim = M.dim;
         const double* omega = P.quad[d].dir;
@@ -1624,6 +1792,9 @@ struct orc_problem {
     int check_rcond;
     int num_active;           // 0: all ordinates
     const int* active;        // ordinates to set up (C4/C5 sampled parity)
+    int face_rule;            // 0 gauss, 1 romberg
+    double romberg_tol;
+    int romberg_max_levels, romberg_min_levels;
 };
 
 static thread_local std::string g_err;
@@ -1665,6 +1836,12 @@ void* orc_create(const orc_problem* p, char* err, int errlen) {
         P.source.inflow = p->inflow;
         P.vol_points = p->volume_points;
         P.face_points = p->face_points;
+        P.face_rule = p->face_rule;
+        if (p->face_rule == 1) {
+            P.romberg_tol = p->romberg_tol;
+            P.romberg_max_levels = p->romberg_max_levels;
+            P.romberg_min_levels = p->romberg_min_levels;
+        }
         P.weighting = p->weighting;
         P.fas_threshold = p->fas_threshold;
         auto* o = new orc::Oracle(std::move(P), p->cache_lu != 0);

@@ -193,8 +193,12 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
     if (ctid == 0) { flg[0] = 0; flg[1] = 0; }
     pair_sync();
     int outm = 0, inm = 0;
+    // Romberg face rule (2D): face blocks integrated at create (assembly.hpp:121-131)
+    const bool romb = DIM == 2 && pr.rom_ob != nullptr;
+    const size_t rfb = ((size_t)d * pr.nel + e) * NF;
     if (!(dbg & 1)) {
-        for (int idx = ctid; idx < NF * NQF; idx += gthreads) {
+        if (romb && ctid == 0) outm = (int)pr.rom_omask[(size_t)d * pr.nel + e];
+        for (int idx = ctid; idx < (romb ? 0 : NF * NQF); idx += gthreads) {
             const int f = idx / NQF, qq = idx - (idx / NQF) * NQF;
             const double4 gm = reinterpret_cast<const double4*>(pr.fgeom)[((size_t)e * NF + f) * NQF + qq];
             double on = om0 * gm.x + om1 * gm.y;
@@ -231,7 +235,7 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
         pair_sync();
         outm = flg[0];
         inm = flg[1];
-        for (int idx = ctid; idx < NF * NQF; idx += gthreads) {
+        for (int idx = ctid; idx < (romb ? 0 : NF * NQF); idx += gthreads) {
             const int f = idx / NQF, qq = idx - (idx / NQF) * NQF;
             double t = 0.0;
             if ((inm >> f) & 1) {
@@ -242,7 +246,7 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
             }
             TR[idx] = t * WI[idx];
         }
-        if (DIM == 3) {
+        if (DIM == 3 && !romb) {
             for (int idx = ctid; idx < NF * T1SZ; idx += gthreads) {
                 const int f = idx / (T1SZ > 0 ? T1SZ : 1), rem = idx - f * T1SZ;
                 if (!((outm >> f) & 1)) continue;
@@ -261,7 +265,9 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
             if (!((outm >> f) & 1)) continue;
             const int fa = rem / NFN, fb = rem - fa * NFN;
             double s = 0.0;
-            if (DIM == 3) {
+            if (romb) {
+                s = pr.rom_ob[(rfb + f) * NFN * NFN + rem];
+            } else if (DIM == 3) {
                 const int a0 = fa % N1, b0 = fa / N1, a1 = fb % N1, b1 = fb / N1;
 #pragma unroll
                 for (int jq = 0; jq < NQ1; ++jq)
@@ -299,7 +305,16 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
                         m &= m - 1;
                         const int fr = s_fidx[f * N + r];
                         double s2 = 0.0;
-                        for (int qq = 0; qq < NQF; ++qq) s2 += TR[f * NQF + qq] * s_trace[qq * NFN + fr];
+                        if (romb) {   // coupling block times the gathered upwind traces, or the inflow moments
+                            if ((inm >> f) & 1) {
+                                const double* ib = pr.rom_ib + ((rfb + f) * NFN + fr) * NFN;
+                                for (int aa = 0; aa < NFN; ++aa) s2 += ib[aa] * UP[f * NFN + aa];
+                            } else {
+                                s2 = pr.rom_bin[(rfb + f) * NFN + fr];
+                            }
+                        } else {
+                            for (int qq = 0; qq < NQF; ++qq) s2 += TR[f * NQF + qq] * s_trace[qq * NFN + fr];
+                        }
                         acc[j][tr][s] += s2;
                     }
                 }

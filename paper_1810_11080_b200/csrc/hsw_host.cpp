@@ -828,6 +828,59 @@ static void lu_solve(const std::vector<double>& a, const std::vector<int>& perm,
 // =================================================================== setup
 struct Coupling { int face, down, up, down_face, up_face; };
 
+// romberg.hpp:33-88: Romberg tableau over successive trapezoid halvings of [0,1] for a
+// vector integrand f(t, out[nv]) sharing one sampling; converged when two successive
+// diagonal entries agree to tol in the max norm, never before min_levels halvings.
+// Coefficient-wise in the reference's order (its Eigen expressions are elementwise);
+// returns the last diagonal entry and whether it converged.
+template <typename F>
+static bool romberg_integrate(F&& f, size_t nv, double tol, int max_levels, int min_levels,
+                              std::vector<double>& out) {
+    min_levels = std::min(min_levels, max_levels);
+    auto finite = [&](const std::vector<double>& v) {
+        for (double x : v)
+            if (std::isnan(x)) throw Error(HSW_ERR_ASSEMBLY, "romberg: integrand returned NaN");
+    };
+    std::vector<double> f0(nv), f1(nv), trap(nv), sum(nv), fi(nv);
+    f(0.0, f0.data());
+    f(1.0, f1.data());
+    finite(f0);
+    finite(f1);
+    for (size_t i = 0; i < nv; ++i) trap[i] = 0.5 * (f0[i] + f1[i]);
+    std::vector<std::vector<double>> diag{trap}, row;
+    bool conv = false;
+    long n = 1;
+    for (int k = 1; k <= max_levels; ++k) {
+        const double h = 1.0 / (2.0 * n);
+        f(h, sum.data());
+        finite(sum);
+        for (long i = 1; i < n; ++i) {
+            f((2 * i + 1) * h, fi.data());
+            finite(fi);
+            for (size_t j = 0; j < nv; ++j) sum[j] += fi[j];
+        }
+        for (size_t j = 0; j < nv; ++j) trap[j] = 0.5 * trap[j] + h * sum[j];
+        n *= 2;
+        row.resize((size_t)k + 1);
+        row[0] = trap;
+        double pow4 = 1.0;
+        for (int j = 1; j <= k; ++j) {
+            pow4 *= 4.0;
+            row[j].resize(nv);
+            for (size_t i = 0; i < nv; ++i) row[j][i] = row[j - 1][i] + (row[j - 1][i] - diag[j - 1][i]) / (pow4 - 1.0);
+        }
+        double diff = 0.0;
+        for (size_t i = 0; i < nv; ++i) diff = std::max(diff, std::abs(row[k][i] - diag[k - 1][i]));
+        diag.swap(row);
+        if (diff < tol && k >= min_levels) {
+            conv = true;
+            break;
+        }
+    }
+    out = diag.back();
+    return conv;
+}
+
 struct Setup {
     // inputs
     int dim = 2, p = 1, nb = 4, nfn = 2, nf = 4, nel = 0, nd = 0;
@@ -839,6 +892,17 @@ struct Setup {
     double source_params[8] = {0};
     double inflow = 0.0;
     int vol_pts = 0, face_pts = 0, weighting = 1, fas_thr = 10;
+    // FaceIntegration (assembly.hpp:33-40): Gauss (face_pts) or Romberg (2D)
+    int face_rule = HSW_FACE_GAUSS;
+    double rom_tol = 1e-10;
+    int rom_max = 16, rom_min = 6;
+    // Romberg face data per (ordinate, element, local face), computed at create and
+    // uploaded: outflow block (own face nodes x own face nodes), incoming coupling block
+    // (own face nodes x own face-node order of the upwind traces, as the kernels gather
+    // them), boundary inflow moments, outflow-face mask
+    std::vector<double> rom_ob, rom_ib, rom_bin;
+    std::vector<uint8_t> rom_omask;
+    std::vector<int> rom_unconverged;   // per ordinate (TransportOperator::PerOrdinate, assembly.hpp:349)
     // quadrature
     Rule line_v, line_f;
     std::vector<std::array<double, 3>> vq_pts;
@@ -933,6 +997,15 @@ struct Setup {
         face_pts = D->face_points > 0 ? D->face_points : p + 2;
         weighting = D->weighting;
         fas_thr = D->exact_fas_threshold > 0 ? D->exact_fas_threshold : 10;
+        face_rule = D->face_rule;
+        if (face_rule != HSW_FACE_GAUSS && face_rule != HSW_FACE_ROMBERG)
+            throw Error(HSW_ERR_INVALID, "hsw_create: unknown face rule");
+        if (face_rule == HSW_FACE_ROMBERG) {
+            if (dim != 2) throw Error(HSW_ERR_INVALID, "romberg face rule: 2D meshes only (the reference is 2D)");
+            rom_tol = D->romberg_tol > 0.0 ? D->romberg_tol : 1e-10;
+            rom_max = D->romberg_max_levels > 0 ? D->romberg_max_levels : 16;
+            rom_min = D->romberg_min_levels >= 0 ? D->romberg_min_levels : 6;
+        }
         basis = TensorBasis(dim, p);
         nb = basis.nb;
         nf = nfaces_of(dim);
@@ -1199,14 +1272,102 @@ struct Setup {
         ords.assign(nd, {});
         inflags.assign((size_t)nd * nel, 0);
         const int nfi = (int)mesh.ifaces.size();
+        const bool romb = face_rule == HSW_FACE_ROMBERG;
+        const size_t nn = (size_t)nfn * nfn;
+        if (romb) {
+            rom_ob.assign((size_t)nd * nel * nf * nn, 0.0);
+            rom_ib.assign((size_t)nd * nel * nf * nn, 0.0);
+            rom_bin.assign((size_t)nd * nel * nf * nfn, 0.0);
+            rom_omask.assign((size_t)nd * nel, 0);
+            rom_unconverged.assign(nd, 0);
+        }
         parallel_for(nd, [&](int64_t d64) {
             const int d = (int)d64;
             const double* om = &odir[3 * d];
             std::vector<double> LR((size_t)nfn * nfn), RL((size_t)nfn * nfn), wp(nqf), wm(nqf);
             auto& cpl = couplings[d];
             auto& wts = weights[d];
+            // Romberg sampling of one face at parameter t (assembly.hpp:103-117): geometry of
+            // the (left) element's face, its face-node traces, the neighbour's at t or 1 - t
+            std::vector<double> gg((size_t)mesh.npe * dim), full(nb), ul(nfn), ur(nfn), packed;
+            auto sample = [&](int e, int f, double t, double& on, double& sj, double* u) {
+                double xi[3], n[3];
+                param_point(dim, f, t, 0.0, xi);
+                mesh.geom.gradients(xi, gg.data());
+                mesh.face_geometry_tab(e, f, gg.data(), n, sj);
+                on = om[0] * n[0] + om[1] * n[1];
+                basis.values(xi, full.data());
+                for (int a = 0; a < nfn; ++a) u[a] = full[fnodes[f][a]];
+            };
+            auto trace_at = [&](int f, double s0, double* u) {
+                double xi[3];
+                param_point(dim, f, s0, 0.0, xi);
+                basis.values(xi, full.data());
+                for (int a = 0; a < nfn; ++a) u[a] = full[fnodes[f][a]];
+            };
+            // incoming block of (downwind element e, face f): columns in e's face-node
+            // order of the gathered upwind traces (kernel: neighbour node P - a if reversed)
+            auto put_in = [&](int e, int f, const double* blk) {
+                const int code = fnbr[((size_t)e * nf + f) * 4 + 2];
+                double* dst = &rom_ib[(((size_t)d * nel + e) * nf + f) * nn];
+                for (int a = 0; a < nfn; ++a)
+                    for (int aa = 0; aa < nfn; ++aa) dst[(size_t)a * nfn + aa] = blk[(size_t)a * nfn + (code ? p - aa : aa)];
+            };
+            auto put_out = [&](int e, int f, const double* blk) {
+                double* dst = &rom_ob[(((size_t)d * nel + e) * nf + f) * nn];
+                bool nz = false;
+                for (size_t k = 0; k < nn; ++k) {
+                    dst[k] = blk[k];
+                    nz |= blk[k] != 0.0;
+                }
+                if (nz) rom_omask[(size_t)d * nel + e] |= (uint8_t)(1u << f);
+            };
             for (int fi = 0; fi < nfi; ++fi) {
                 const IFace& F = mesh.ifaces[fi];
+                if (romb) {   // assembly.hpp:195-241 with FaceIntegration::Rule::romberg
+                    auto integrand = [&](double t, double* v) {
+                        double on, sj, so, to;
+                        sample(F.el, F.fl, t, on, sj, ul.data());
+                        orient_param(dim, F.orient, t, 0.0, so, to);
+                        trace_at(F.fr, so, ur.data());
+                        const double wplus = 0.5 * (on + std::abs(on));
+                        const double wminus = 0.5 * (std::abs(on) - on);
+                        size_t k = 0;
+                        for (int m = 0; m < nfn; ++m)
+                            for (int n = 0; n < nfn; ++n) v[k++] = wplus * ul[m] * ul[n] * sj;
+                        for (int m = 0; m < nfn; ++m)
+                            for (int n = 0; n < nfn; ++n) v[k++] = wminus * ur[m] * ur[n] * sj;
+                        for (int m = 0; m < nfn; ++m)
+                            for (int n = 0; n < nfn; ++n) v[k++] = wminus * ul[m] * ur[n] * sj;
+                        for (int m = 0; m < nfn; ++m)
+                            for (int n = 0; n < nfn; ++n) v[k++] = wplus * ur[m] * ul[n] * sj;
+                        v[k] = sj;
+                    };
+                    if (!romberg_integrate(integrand, 4 * nn + 1, rom_tol, rom_max, rom_min, packed))
+                        rom_unconverged[d]++;
+                    const double length = packed[4 * nn];
+                    const double eps = 1e-12 * length;
+                    put_out(F.el, F.fl, &packed[0]);
+                    put_out(F.er, F.fr, &packed[nn]);
+                    std::copy(packed.begin() + 2 * nn, packed.begin() + 3 * nn, LR.begin());
+                    std::copy(packed.begin() + 3 * nn, packed.begin() + 4 * nn, RL.begin());
+                    double mlr = 0.0, mrl = 0.0;
+                    for (size_t k = 0; k < nn; ++k) {
+                        mlr = std::max(mlr, std::abs(LR[k]));
+                        mrl = std::max(mrl, std::abs(RL[k]));
+                    }
+                    if (mlr > eps) {
+                        cpl.push_back({fi, F.el, F.er, F.fl, F.fr});
+                        wts.push_back(weight_of(mlr, F.el, F.fl, LR, false));
+                        put_in(F.el, F.fl, LR.data());
+                    }
+                    if (mrl > eps) {
+                        cpl.push_back({fi, F.er, F.el, F.fr, F.fl});
+                        wts.push_back(weight_of(mrl, F.er, F.fr, RL, false));
+                        put_in(F.er, F.fr, RL.data());
+                    }
+                    continue;
+                }
                 const double* geo = &fgeom[(((size_t)F.el * nf + F.fl) * nqf) * 4];
                 const double* sjv = &fsj[((size_t)F.el * nf + F.fl) * nqf];
                 std::fill(LR.begin(), LR.end(), 0.0);
@@ -1264,6 +1425,34 @@ struct Setup {
                     cpl.push_back({fi, F.er, F.el, F.fr, F.fl});
                     wts.push_back(weight_of(mrl, F.er, F.fr, RL, false));
                 }
+            }
+            if (romb) {   // boundary outflow (assembly.hpp:244-266), then the inflow moments (:302-313)
+                std::vector<double> mom;
+                for (const auto& B : mesh.bfaces) {
+                    auto outflow = [&](double t, double* v) {
+                        double on, sj;
+                        sample(B.elem, B.face, t, on, sj, ul.data());
+                        const double wplus = 0.5 * (on + std::abs(on));
+                        size_t k = 0;
+                        for (int m = 0; m < nfn; ++m)
+                            for (int n = 0; n < nfn; ++n) v[k++] = wplus * ul[m] * ul[n] * sj;
+                    };
+                    if (!romberg_integrate(outflow, nn, rom_tol, rom_max, rom_min, packed)) rom_unconverged[d]++;
+                    put_out(B.elem, B.face, packed.data());
+                }
+                if (inflow != 0.0)
+                    for (const auto& B : mesh.bfaces) {
+                        auto incident = [&](double t, double* v) {
+                            double on, sj;
+                            sample(B.elem, B.face, t, on, sj, ul.data());
+                            const double wminus = 0.5 * (std::abs(on) - on);
+                            const double c = wminus * inflow * sj;
+                            for (int m = 0; m < nfn; ++m) v[m] = c * ul[m];
+                        };
+                        romberg_integrate(incident, (size_t)nfn, rom_tol, rom_max, rom_min, mom);
+                        double* dst = &rom_bin[(((size_t)d * nel + B.elem) * nf + B.face) * nfn];
+                        for (int m = 0; m < nfn; ++m) dst[m] += mom[m];
+                    }
             }
             std::vector<Edge> edges(cpl.size());
             for (size_t c = 0; c < cpl.size(); ++c) edges[c] = {cpl[c].up, cpl[c].down, wts[c]};
@@ -1367,6 +1556,8 @@ struct hsw_handle {
     cudaStream_t stream = nullptr;
     DevProblem P{};
     // device buffers
+    double *d_rom_ob = nullptr, *d_rom_ib = nullptr, *d_rom_bin = nullptr;
+    unsigned char* d_rom_omask = nullptr;
     double *d_T = nullptr, *d_sig_t = nullptr, *d_sig_s = nullptr, *d_qvol = nullptr, *d_fgeom = nullptr;
     double* d_bscale = nullptr;
     int* d_fnbr = nullptr;
@@ -1467,7 +1658,8 @@ void free_handle(hsw_handle* h) {
     void* bufs[] = {h->d_T, h->d_sig_t, h->d_bscale, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
                     h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
-                    h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line};
+                    h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line,
+                    h->d_rom_ob, h->d_rom_ib, h->d_rom_bin, h->d_rom_omask};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& kv : h->ranges)
@@ -1868,7 +2060,8 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         phase("face_tables");
         if (desc->device >= 0) {
             device_init(h, desc->device);
-            if (S.weighting != HSW_WEIGHT_SIGINVFACE) {   // siginvface needs the blocks on the host
+            if (S.weighting != HSW_WEIGHT_SIGINVFACE && S.face_rule == HSW_FACE_GAUSS) {
+                // (siginvface needs the blocks on the host; Romberg integrates them there)
                 device_coupling_max(h);
                 phase("couplings(dev)");
             }
@@ -1991,6 +2184,17 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             const char* tv = std::getenv("HSW_TUNE");
             P.tune = tv ? std::atoi(tv) : 0;
         }
+        if (S.face_rule == HSW_FACE_ROMBERG) {
+            h->d_rom_ob = dev_upload(S.rom_ob);
+            h->d_rom_ib = dev_upload(S.rom_ib);
+            h->d_rom_bin = dev_upload(S.rom_bin);
+            std::vector<unsigned char> om(S.rom_omask.begin(), S.rom_omask.end());
+            h->d_rom_omask = dev_upload(om);
+        }
+        P.rom_ob = h->d_rom_ob;
+        P.rom_ib = h->d_rom_ib;
+        P.rom_bin = h->d_rom_bin;
+        P.rom_omask = h->d_rom_omask;
         P.T = h->d_T; P.sig_t = h->d_sig_t; P.bscale = h->d_bscale; P.sig_s = h->d_sig_s; P.qvol = h->d_qvol;
         P.fgeom = h->d_fgeom; P.fnbr = h->d_fnbr; P.inflags = h->d_inflags;
         P.omega = h->d_omega; P.weight = h->d_weight; P.inflow = S.inflow;
@@ -2440,6 +2644,20 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
                 const double* geo = &S.fgeom[(((size_t)B.elem * S.nf + B.face) * nqf) * 4];
                 const double* psie = psi + (size_t)d * N + (size_t)B.elem * nb;
                 double o = 0.0;
+                if (S.face_rule == HSW_FACE_ROMBERG) {   // the integrated blocks (solver.hpp:225-233)
+                    const size_t fb = ((size_t)d * S.nel + B.elem) * S.nf + B.face;
+                    const double* blk = &S.rom_ob[fb * nfn * nfn];
+                    for (int m = 0; m < nfn; ++m) {
+                        double r = 0.0;
+                        for (int n = 0; n < nfn; ++n) r += blk[(size_t)m * nfn + n] * psie[S.fnodes[B.face][n]];
+                        o += r;
+                    }
+                    for (int m = 0; m < nfn; ++m) inf_d += S.rom_bin[fb * nfn + m];
+                    o *= w;
+                    outflow += o;
+                    by_attr[B.attr] += o;
+                    continue;
+                }
                 for (int q = 0; q < nqf; ++q) {
                     double on = 0.0;
                     for (int k = 0; k < S.dim; ++k) on += om[k] * geo[q * 4 + k];

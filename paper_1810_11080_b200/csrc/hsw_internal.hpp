@@ -74,6 +74,13 @@ struct DevProblem {
                               // profiling instantiations only)
     unsigned long long* prof; // [16] debug phase-cycle accumulators
     int tune;                 // development knobs (HSW_TUNE, bit flags; 0 = production defaults)
+    // FaceIntegration::Rule::romberg (2D; null with the Gauss rule): per (ordinate, element,
+    // local face) blocks integrated at create (assembly.hpp:121-131, romberg.hpp)
+    const double* rom_ob;     // [nd][E][nf][nfn*nfn] outflow block, own face nodes
+    const double* rom_ib;     // [nd][E][nf][nfn*nfn] incoming coupling block (positive integral;
+                              // columns in own face-node order of the gathered upwind traces)
+    const double* rom_bin;    // [nd][E][nf][nfn] boundary inflow moments
+    const unsigned char* rom_omask;   // [nd][E] faces with a nonzero outflow block
 };
 
 // Host-computed reference-face tables (uploaded as the g_* global tables).

@@ -55,6 +55,10 @@ class Problem:
     inflow: float = 0.0         # isotropic incident flux (SourceSpec::isotropic)
     volume_points: int = 0      # 0 -> p + 2 per axis (assembly.hpp:146)
     face_points: int = 0        # 0 -> p + 2 Gauss points per face axis
+    face_rule: int = 0          # FaceIntegration::Rule (assembly.hpp:33-40): 0 gauss, 1 romberg (2D)
+    romberg_tol: float = 1e-10  # FaceIntegration defaults (assembly.hpp:36-38)
+    romberg_max_levels: int = 16
+    romberg_min_levels: int = 6
     weighting: int = 1          # 0 unity, 1 face (default), 2 siginvface
     fas_threshold: int = 10     # exact FAS up to this SCC size (solver.hpp:31)
     name: str = "custom"

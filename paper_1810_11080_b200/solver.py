@@ -188,6 +188,10 @@ class SweepSolver:
         # for a singular one (solver.hpp:67-75): on by default here too
         d.check_local_blocks = int(check_local_blocks)
         d.device = device  # < 0: host-only plan (graphs/orderings, no device state)
+        d.face_rule = int(getattr(problem, "face_rule", 0))
+        d.romberg_tol = float(getattr(problem, "romberg_tol", 1e-10))
+        d.romberg_max_levels = int(getattr(problem, "romberg_max_levels", 16))
+        d.romberg_min_levels = int(getattr(problem, "romberg_min_levels", 6))
         h = C.c_void_p()
         _check(L.hsw_create(C.byref(d), C.byref(h)))
         self._h = h

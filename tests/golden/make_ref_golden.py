@@ -32,6 +32,10 @@ CASES = [
     ("ref_c1", ("c1", {}), {}, 1e-12, 400, 16),
     ("ref_c1_inflow", ("c1", dict(cells=4)), dict(inflow=0.7), 1e-12, 400, 16),
     ("ref_c2_small", ("c2", dict(cells=16, n_mu=2, n_az=8)), {}, 1e-12, 400, 0),
+    # the reference's DEFAULT face rule: Romberg (assembly.hpp:33-40, romberg.hpp)
+    ("ref_c1_romberg", ("c1", {}), dict(face_rule=1), 1e-12, 400, 16),
+    ("ref_c1_romberg_inflow", ("c1", dict(cells=4)), dict(face_rule=1, inflow=0.7), 1e-12, 400, 16),
+    ("ref_c2_small_romberg", ("c2", dict(cells=12, n_mu=2, n_az=8)), dict(face_rule=1), 1e-12, 400, 0),
 ]
 
 
@@ -76,7 +80,7 @@ def main():
         prob = pb.config(cfg, **kw)
         if extra:
             prob = prob.replace(**extra)
-        out = run_case(prob, tol, mx, ndir)
+        out = run_case(prob, tol, mx, ndir, face_rule=prob.face_rule)
         out["case"] = np.array(repr((cfg, kw, extra, tol, mx, ndir)))
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
         print(name, {k: v.shape for k, v in out.items() if hasattr(v, "shape")})

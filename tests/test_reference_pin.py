@@ -28,6 +28,10 @@ CASES = {
     "ref_c1": ("c1", {}, {}),
     "ref_c1_inflow": ("c1", dict(cells=4), dict(inflow=0.7)),
     "ref_c2_small": ("c2", dict(cells=16, n_mu=2, n_az=8), {}),
+    # FaceIntegration::Rule::romberg, the reference's default (assembly.hpp:33-40)
+    "ref_c1_romberg": ("c1", {}, dict(face_rule=1)),
+    "ref_c1_romberg_inflow": ("c1", dict(cells=4), dict(face_rule=1, inflow=0.7)),
+    "ref_c2_small_romberg": ("c2", dict(cells=12, n_mu=2, n_az=8), dict(face_rule=1)),
 }
 
 
@@ -93,7 +97,7 @@ def test_oracle_equals_reference(name):
     r = orc.source_iteration(1e-12, 400, 0)
     assert r["converged"] and conv and r["iterations"] == its
     assert rel_l2(r["phi"], g["si_phi"]) <= 1e-12 and rel_l2(r["psi"], g["si_psi"].reshape(nd, N)) <= 1e-12
-    np.testing.assert_allclose(r["error"], g["si_error"], rtol=1e-6, atol=1e-15)
+    np.testing.assert_allclose(r["error"], g["si_error"], rtol=1e-6, atol=1e-14)   # last entries: round-off level
     b = orc.balance(g["si_psi"].reshape(nd, N), g["si_phi"])
     for k, v in zip(("source_volume", "inflow", "absorption", "outflow"), g["balance"][:4]):
         assert abs(b[k] - v) <= 1e-12 * max(abs(v), 1.0), k
