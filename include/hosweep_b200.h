@@ -193,6 +193,11 @@ int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_resul
  * attribute (up to cap entries, *count true count). */
 int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5[5], int* attrs,
                 double* vals, int cap, int* count);
+/* balance_report of the handle's RESIDENT state (after hsw_source_iteration: its
+ * converged psi / phi; after hsw_set_state: the state set), evaluated on the
+ * device: per boundary face a deterministic sum over the ordinates, absorption
+ * by a fixed-shape reduction.  Same outputs as hsw_balance. */
+int hsw_balance_resident(hsw_handle* h, double out5[5], int* attrs, double* vals, int cap, int* count);
 
 /* ---- device-resident state for benchmarking / advanced callers ---------- */
 /* Device pointers of the handle's psi (two buffers, [nd][N] each) and phi. */

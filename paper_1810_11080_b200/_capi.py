@@ -25,7 +25,7 @@ EXPORTED = [
     "hsw_last_error", "hsw_create", "hsw_destroy", "hsw_sizes", "hsw_ordering",
     "hsw_total_lagged_edges", "hsw_couplings", "hsw_interior_faces", "hsw_local_solve",
     "hsw_sweep", "hsw_sweep_device", "hsw_direct_oracle", "hsw_source_iteration", "hsw_balance",
-    "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
+    "hsw_balance_resident", "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
     "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
     "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
     "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_sweep_host", "hsw_shard_phi_partial", "hsw_shard_psi_error",
@@ -88,6 +88,7 @@ def load():
     L.hsw_direct_oracle.argtypes = [vp, C.c_int, vp, vp]
     L.hsw_source_iteration.argtypes = [vp, C.POINTER(hsw_si_options), C.POINTER(hsw_si_result), vp, vp, vp, vp, vp]
     L.hsw_balance.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, vp]
+    L.hsw_balance_resident.argtypes = [vp, vp, vp, vp, C.c_int, vp]
     L.hsw_device_state.argtypes = [vp, vp, vp, vp]
     L.hsw_sweep_resident.argtypes = [vp]
     L.hsw_synchronize.argtypes = [vp]

@@ -1263,6 +1263,10 @@ struct Setup {
             }
     }
 
+    // face blocks integrated on the host for the kernels (2D): Romberg, or a Gauss rule with
+    // other than the kernels' p + 2 points per face
+    bool face_blocks() const { return face_rule == HSW_FACE_ROMBERG || (dim == 2 && face_pts != p + 2); }
+
     // assembly.hpp:185-241 (interior faces, Gauss rule) -> couplings + weights,
     // then sweepgraph.hpp:54-77 + 331-396, lag flags (solver.hpp:63-66) and levels.
     void ordinates() {
@@ -1272,7 +1276,10 @@ struct Setup {
         ords.assign(nd, {});
         inflags.assign((size_t)nd * nel, 0);
         const int nfi = (int)mesh.ifaces.size();
-        const bool romb = face_rule == HSW_FACE_ROMBERG;
+        // face blocks integrated here and handed to the kernels (2D): the Romberg rule, or a
+        // Gauss rule other than the kernels' own p + 2 points (the reference's gauss_points)
+        const bool romb = face_blocks();
+        const bool use_romberg = face_rule == HSW_FACE_ROMBERG;
         const size_t nn = (size_t)nfn * nfn;
         if (romb) {
             rom_ob.assign((size_t)nd * nel * nf * nn, 0.0);
@@ -1289,7 +1296,18 @@ struct Setup {
             auto& wts = weights[d];
             // Romberg sampling of one face at parameter t (assembly.hpp:103-117): geometry of
             // the (left) element's face, its face-node traces, the neighbour's at t or 1 - t
-            std::vector<double> gg((size_t)mesh.npe * dim), full(nb), ul(nfn), ur(nfn), packed;
+            std::vector<double> gg((size_t)mesh.npe * dim), full(nb), ul(nfn), ur(nfn), packed, gtmp;
+            // integrate_face (assembly.hpp:121-131): Romberg, or out += w_i f(t_i) over the Gauss rule
+            auto integrate = [&](auto&& fn, size_t nv, std::vector<double>& out) -> bool {
+                if (use_romberg) return romberg_integrate(fn, nv, rom_tol, rom_max, rom_min, out);
+                out.assign(nv, 0.0);
+                gtmp.resize(nv);
+                for (int i = 0; i < face_pts; ++i) {
+                    fn(line_f.x[i], gtmp.data());
+                    for (size_t j = 0; j < nv; ++j) out[j] += line_f.w[i] * gtmp[j];
+                }
+                return true;
+            };
             auto sample = [&](int e, int f, double t, double& on, double& sj, double* u) {
                 double xi[3], n[3];
                 param_point(dim, f, t, 0.0, xi);
@@ -1343,8 +1361,7 @@ struct Setup {
                             for (int n = 0; n < nfn; ++n) v[k++] = wplus * ur[m] * ul[n] * sj;
                         v[k] = sj;
                     };
-                    if (!romberg_integrate(integrand, 4 * nn + 1, rom_tol, rom_max, rom_min, packed))
-                        rom_unconverged[d]++;
+                    if (!integrate(integrand, 4 * nn + 1, packed)) rom_unconverged[d]++;
                     const double length = packed[4 * nn];
                     const double eps = 1e-12 * length;
                     put_out(F.el, F.fl, &packed[0]);
@@ -1437,7 +1454,7 @@ struct Setup {
                         for (int m = 0; m < nfn; ++m)
                             for (int n = 0; n < nfn; ++n) v[k++] = wplus * ul[m] * ul[n] * sj;
                     };
-                    if (!romberg_integrate(outflow, nn, rom_tol, rom_max, rom_min, packed)) rom_unconverged[d]++;
+                    if (!integrate(outflow, nn, packed)) rom_unconverged[d]++;
                     put_out(B.elem, B.face, packed.data());
                 }
                 if (inflow != 0.0)
@@ -1449,7 +1466,7 @@ struct Setup {
                             const double c = wminus * inflow * sj;
                             for (int m = 0; m < nfn; ++m) v[m] = c * ul[m];
                         };
-                        romberg_integrate(incident, (size_t)nfn, rom_tol, rom_max, rom_min, mom);
+                        integrate(incident, (size_t)nfn, mom);
                         double* dst = &rom_bin[(((size_t)d * nel + B.elem) * nf + B.face) * nfn];
                         for (int m = 0; m < nfn; ++m) dst[m] += mom[m];
                     }
@@ -1557,6 +1574,7 @@ struct hsw_handle {
     DevProblem P{};
     // device buffers
     double *d_rom_ob = nullptr, *d_rom_ib = nullptr, *d_rom_bin = nullptr;
+    int* d_bfaces = nullptr;   // (elem, face, attr) per boundary face, for the device balance
     unsigned char* d_rom_omask = nullptr;
     double *d_T = nullptr, *d_sig_t = nullptr, *d_sig_s = nullptr, *d_qvol = nullptr, *d_fgeom = nullptr;
     double* d_bscale = nullptr;
@@ -1659,7 +1677,7 @@ void free_handle(hsw_handle* h) {
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
                     h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
                     h->d_err, h->d_prof, h->d_tab_fnode, h->d_tab_fidx, h->d_tab_nmask, h->d_tab_trace, h->d_tab_line,
-                    h->d_rom_ob, h->d_rom_ib, h->d_rom_bin, h->d_rom_omask};
+                    h->d_rom_ob, h->d_rom_ib, h->d_rom_bin, h->d_rom_omask, h->d_bfaces};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (auto& kv : h->ranges)
@@ -2060,7 +2078,10 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         phase("face_tables");
         if (desc->device >= 0) {
             device_init(h, desc->device);
-            if (S.weighting != HSW_WEIGHT_SIGINVFACE && S.face_rule == HSW_FACE_GAUSS) {
+            if (S.dim == 3 && S.face_pts != S.p + 2)
+                throw hsw::Error(HSW_ERR_INVALID, "hsw_create: the 3D kernels integrate faces with p + 2 Gauss "
+                                                  "points per axis (face_points " + std::to_string(S.face_pts) + ")");
+            if (S.weighting != HSW_WEIGHT_SIGINVFACE && !S.face_blocks()) {
                 // (siginvface needs the blocks on the host; Romberg integrates them there)
                 device_coupling_max(h);
                 phase("couplings(dev)");
@@ -2184,7 +2205,7 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             const char* tv = std::getenv("HSW_TUNE");
             P.tune = tv ? std::atoi(tv) : 0;
         }
-        if (S.face_rule == HSW_FACE_ROMBERG) {
+        if (S.face_blocks()) {
             h->d_rom_ob = dev_upload(S.rom_ob);
             h->d_rom_ib = dev_upload(S.rom_ib);
             h->d_rom_bin = dev_upload(S.rom_bin);
@@ -2644,7 +2665,7 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
                 const double* geo = &S.fgeom[(((size_t)B.elem * S.nf + B.face) * nqf) * 4];
                 const double* psie = psi + (size_t)d * N + (size_t)B.elem * nb;
                 double o = 0.0;
-                if (S.face_rule == HSW_FACE_ROMBERG) {   // the integrated blocks (solver.hpp:225-233)
+                if (S.face_blocks()) {   // the integrated blocks (solver.hpp:225-233)
                     const size_t fb = ((size_t)d * S.nel + B.elem) * S.nf + B.face;
                     const double* blk = &S.rom_ob[fb * nfn * nfn];
                     for (int m = 0; m < nfn; ++m) {
@@ -2691,6 +2712,59 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
             CUDA_OK(cudaMemcpyAsync(h->d_vec, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
             absorption = dev_absorption(S.nel, nb, h->d_T, h->d_sig_t, h->d_sig_s, h->d_vec, h->d_scratch, h->stream);
         }
+        out5[0] = sv;
+        out5[1] = inflow_tot;
+        out5[2] = absorption;
+        out5[3] = outflow;
+        out5[4] = sv + inflow_tot - absorption - outflow;
+        int k = 0;
+        for (const auto& kv : by_attr) {
+            if (k < cap && attrs && vals) {
+                attrs[k] = kv.first;
+                vals[k] = kv.second;
+            }
+            ++k;
+        }
+        if (count) *count = k;
+        return HSW_OK;
+    });
+}
+
+int hsw_balance_resident(hsw_handle* h, double out5[5], int* attrs, double* vals, int cap, int* count) {
+    return guarded([&] {
+        if (!h || !out5) throw hsw::Error(HSW_ERR_INVALID, "hsw_balance_resident: null argument");
+        HandleScope hs(h);
+        need_device(h);
+        const Setup& S = h->S;
+        const int nbf = (int)S.mesh.bfaces.size();
+        if (!h->d_bfaces && nbf > 0) {
+            std::vector<int> bf((size_t)nbf * 3);
+            for (int i = 0; i < nbf; ++i) {
+                bf[3 * i] = S.mesh.bfaces[i].elem;
+                bf[3 * i + 1] = S.mesh.bfaces[i].face;
+                bf[3 * i + 2] = S.mesh.bfaces[i].attr;
+            }
+            h->d_bfaces = dev_upload(bf);
+        }
+        double* d_out = nullptr;
+        CUDA_OK(cudaMallocAsync(&d_out, (size_t)std::max(nbf, 1) * 2 * sizeof(double), h->stream));
+        dev_balance_faces(h->P, h->d_psiA, nbf, h->d_bfaces, d_out, h->stream);
+        std::vector<double> fo((size_t)nbf * 2);
+        if (nbf > 0)
+            CUDA_OK(cudaMemcpyAsync(fo.data(), d_out, fo.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaFreeAsync(d_out, h->stream));
+        const double absorption =
+            dev_absorption(S.nel, S.nb, h->d_T, h->d_sig_t, h->d_sig_s, h->d_phi, h->d_scratch, h->stream);
+        double qsum = 0.0, wsum = 0.0, outflow = 0.0, inflow_tot = 0.0;
+        for (size_t i = 0; i < h->N; ++i) qsum += S.qvol[i];
+        for (int d = 0; d < S.nd; ++d) wsum += S.ow[d];
+        std::map<int, double> by_attr;
+        for (int i = 0; i < nbf; ++i) {
+            outflow += fo[2 * i];
+            inflow_tot += fo[2 * i + 1];
+            by_attr[S.mesh.bfaces[i].attr] += fo[2 * i];
+        }
+        const double sv = wsum * qsum;
         out5[0] = sv;
         out5[1] = inflow_tot;
         out5[2] = absorption;

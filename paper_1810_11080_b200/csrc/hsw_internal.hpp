@@ -124,6 +124,9 @@ void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double
                          unsigned long long* bad_elem, void* stream);
 double dev_absorption(int nel, int nb, const double* T, const double* sig_t, const double* sig_s, const double* phi,
                       double* scratch, void* stream);
+// per boundary face (elem, face, attr triples): out[2 bi] = sum_d w_d 1^T B psi_d (outflow),
+// out[2 bi + 1] = sum_d w_d * inflow moments (device balance_report, solver.hpp:220-245)
+void dev_balance_faces(const DevProblem& P, const double* psi, int nbf, const int* bfaces, double* out, void* stream);
 void dev_coupling_max(int dim, int nfi, int nf, int nqf, int nfn, const int* iface, const double* fgeom,
                       const double* fsj, const double* fqw, const double* trace, const double* traceR,
                       const double* odir, int d0, int d1, double* out, void* stream);

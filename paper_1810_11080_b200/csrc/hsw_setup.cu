@@ -213,6 +213,62 @@ void dev_element_tensors(int dim, int nel, int nb, int npe, int nq, const double
     SCHECK(cudaGetLastError());
 }
 
+// balance_report's boundary terms on the device (solver.hpp:220-245): per boundary face,
+// summed over the ordinates in ascending order, the outflow w_d 1^T B_d psi_d and the
+// inflow w_d sum(source_boundary_d) — Gauss rule from the face tables (as the kernels
+// assemble B), Romberg rule from the integrated blocks.  One thread per face: fixed order.
+__global__ void __launch_bounds__(128)
+balance_faces_kernel(const DevProblem pr, const double* __restrict__ psi, int nbf, const int* __restrict__ bfaces,
+                     double* __restrict__ out) {
+    const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bi >= nbf) return;
+    const int e = bfaces[3 * bi], f = bfaces[3 * bi + 1];
+    const int nfn = pr.nfn, nqf = pr.nqf, nb = pr.nb;
+    const size_t N = (size_t)pr.nel * nb;
+    double otot = 0.0, itot = 0.0;
+    for (int d = 0; d < pr.nd; ++d) {
+        const double* ps = psi + (size_t)d * N + (size_t)e * nb;
+        double o = 0.0, in = 0.0;
+        if (pr.rom_ob) {
+            const size_t fb = ((size_t)d * pr.nel + e) * pr.nfaces + f;
+            const double* blk = pr.rom_ob + fb * nfn * nfn;
+            for (int m = 0; m < nfn; ++m) {
+                double r = 0.0;
+                for (int n = 0; n < nfn; ++n) r += blk[m * nfn + n] * ps[pr.g_fnode[f * kMaxFaceNodes + n]];
+                o += r;
+            }
+            for (int m = 0; m < nfn; ++m) in += pr.rom_bin[fb * nfn + m];
+        } else {
+            const double* om = pr.omega + 4 * d;
+            const double4* geo = reinterpret_cast<const double4*>(pr.fgeom) + ((size_t)e * pr.nfaces + f) * nqf;
+            for (int q = 0; q < nqf; ++q) {
+                const double4 gm = geo[q];
+                double on = om[0] * gm.x + om[1] * gm.y;
+                if (pr.dim == 3) on += om[2] * gm.z;
+                const double wplus = 0.5 * (on + fabs(on)), wminus = 0.5 * (fabs(on) - on);
+                double tr = 0.0, ts = 0.0;
+                for (int a = 0; a < nfn; ++a) {
+                    const double t = pr.g_trace[q * kMaxFaceNodes + a];
+                    tr += t * ps[pr.g_fnode[f * kMaxFaceNodes + a]];
+                    ts += t;
+                }
+                o += gm.w * wplus * tr * ts;
+                in += gm.w * wminus * pr.inflow * ts;
+            }
+        }
+        otot += pr.weight[d] * o;
+        itot += pr.weight[d] * in;
+    }
+    out[2 * bi] = otot;
+    out[2 * bi + 1] = itot;
+}
+
+void dev_balance_faces(const DevProblem& P, const double* psi, int nbf, const int* bfaces, double* out, void* stream) {
+    if (nbf <= 0) return;
+    balance_faces_kernel<<<(nbf + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P, psi, nbf, bfaces, out);
+    SCHECK(cudaGetLastError());
+}
+
 double dev_absorption(int nel, int nb, const double* T, const double* sig_t, const double* sig_s, const double* phi,
                       double* scratch, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;

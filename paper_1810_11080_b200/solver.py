@@ -268,6 +268,7 @@ class SweepSolver:
         (num_ordinates, num_dofs)).  ``out`` (optional, C-contiguous float64 of psi_old's
         shape, not aliasing it) receives the result instead of a freshly allocated array:
         a fresh multi-GB array pays the OS's first-touch page faults on every call."""
+        self._last_si_state = None   # the device psi buffers are reused by this call
         phi = np.ascontiguousarray(phi, np.float64)
         psi_old = np.ascontiguousarray(psi_old, np.float64)
         if out is None:
@@ -279,6 +280,7 @@ class SweepSolver:
         return out
 
     def direct_oracle(self, d: int, phi) -> np.ndarray:
+        self._last_si_state = None
         phi = np.ascontiguousarray(phi, np.float64)
         out = np.zeros(self.num_dofs)
         _check(_capi.load().hsw_direct_oracle(self._h, d, _p(phi), _p(out)))
@@ -299,6 +301,7 @@ class SweepSolver:
                                                  _p(eh), _p(ph), _p(po)))
         it = res.iterations
         state = SolverState(psi, phi, it)
+        self._last_si_state = state   # resident on the device until the next call that moves psi
         hist = ConvergenceHistory(list(eh[:it]), list(ph[:it]), bool(res.converged), res.seconds,
                                   [list(r) for r in po[:it]])
         return state, hist
@@ -314,15 +317,20 @@ class SweepSolver:
         _check(_capi.load().hsw_debug_zero_block(self._h, e, d))
 
 
-def balance_report(solver: SweepSolver, state: SolverState) -> BalanceReport:
+def balance_report(solver: SweepSolver, state: Optional[SolverState] = None) -> BalanceReport:
     """solver.hpp:220-245 conservation functionals of a state."""
     out = np.zeros(5)
     attrs = np.zeros(64, np.int32)
     vals = np.zeros(64)
     cnt = C.c_int()
-    psi = np.ascontiguousarray(state.psi, np.float64)
-    phi = np.ascontiguousarray(state.phi, np.float64)
-    _check(_capi.load().hsw_balance(solver.handle, _p(psi), _p(phi), _p(out), _p(attrs), _p(vals), 64,
-                                    C.byref(cnt)))
+    if state is None or state is getattr(solver, "_last_si_state", None) or state.psi is None:
+        # the solver's own converged state is still resident on the device: evaluate there
+        # (hsw_balance_resident), no 2 x nd x N host round trip
+        _check(_capi.load().hsw_balance_resident(solver.handle, _p(out), _p(attrs), _p(vals), 64, C.byref(cnt)))
+    else:
+        psi = np.ascontiguousarray(state.psi, np.float64)
+        phi = np.ascontiguousarray(state.phi, np.float64)
+        _check(_capi.load().hsw_balance(solver.handle, _p(psi), _p(phi), _p(out), _p(attrs), _p(vals), 64,
+                                        C.byref(cnt)))
     by = {int(attrs[i]): float(vals[i]) for i in range(min(cnt.value, 64))}
     return BalanceReport(out[0], out[1], out[0] + out[1], out[2], out[3], out[3] - out[1], out[4], by)

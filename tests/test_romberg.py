@@ -82,3 +82,44 @@ def test_gpu_romberg_sweep_and_si_match_oracle(name, kw):
     r = orc.source_iteration(1e-12, 400, 0)
     assert hist.converged and hist.iterations() == r["iterations"]
     assert np.linalg.norm(state.phi - r["phi"]) <= 1e-8 * np.linalg.norm(r["phi"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("face_points", [2, 8])
+def test_gpu_gauss_other_point_counts_match_oracle(face_points):
+    """FaceIntegration::gauss_points other than the kernels' own p + 2 (the reference's
+    default is 8): the faces are integrated at create and the kernels take the blocks."""
+    prob = pb.config("c2", cells=10, n_mu=2, n_az=8).replace(face_points=face_points, inflow=0.2)
+    s = pk.SweepSolver(prob)
+    orc = O.OracleSolver(prob)
+    for d in range(prob.num_ordinates):
+        o = s.ordering(d)
+        r = orc.ordering(d)
+        assert (o.order == r["order"]).all() and (o.lagged_edges == r["lagged_edges"]).all()
+    rng = np.random.default_rng(2)
+    phi = rng.uniform(0, 1, prob.num_dofs)
+    psi_old = rng.uniform(0, 1, (prob.num_ordinates, prob.num_dofs))
+    got, ref = s.sweep(-1, phi, psi_old), orc.sweep_all(phi, psi_old)
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,kw,extra", [("c1", {}, dict(face_rule=1, inflow=0.3)),
+                                           ("c3", dict(cells=4, n_mu=2, n_az=4), dict(inflow=0.3)),
+                                           ("c2", dict(cells=12, n_mu=2, n_az=8), {})])
+def test_device_balance_report_matches_oracle(name, kw, extra):
+    """balance_report (solver.hpp:220-245) evaluated on the device from the resident
+    converged state (hsw_balance_resident) against the oracle's and the host path's."""
+    prob = pb.config(name, **kw).replace(**extra)
+    s = pk.SweepSolver(prob, pk.SolveOptions(tolerance=1e-12, max_iterations=3000))
+    state, hist = s.source_iteration()
+    assert hist.converged
+    dev = pk.balance_report(s)                        # resident: device path
+    host = pk.balance_report(s, pk.SolverState(state.psi.copy(), state.phi.copy(), state.iterations))
+    bo = O.OracleSolver(prob).balance(state.psi, state.phi)
+    for k in ("source_volume", "inflow", "absorption", "outflow"):
+        assert abs(getattr(dev, k) - bo[k]) <= 1e-10 * max(abs(bo[k]), 1e-300), k
+        assert abs(getattr(dev, k) - getattr(host, k)) <= 1e-12 * max(abs(bo[k]), 1e-300), k
+    assert abs(dev.residual) <= 1e-8 * bo["source_total"]
+    for a, v in bo["outflow_by_attr"].items():
+        assert abs(dev.outflow_by_attr[a] - v) <= 1e-10 * abs(bo["outflow"])
