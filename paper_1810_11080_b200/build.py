@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-SOURCES_CU = ["hsw_kernels.cu", "hsw_dmma.cu", "hsw_dmma1.cu", "hsw_setup.cu"]
+SOURCES_CU = ["hsw_kernels.cu", "hsw_dmma.cu", "hsw_dmma1.cu", "hsw_dmma2.cu", "hsw_setup.cu"]
 SOURCES_CPP = ["hsw_host.cpp"]
 HEADERS = ["hsw_internal.hpp", os.path.join(ROOT, "include", "hosweep_b200.h")]
 

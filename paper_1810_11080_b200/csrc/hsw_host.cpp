@@ -1736,16 +1736,25 @@ void check_err(hsw_handle* h) {
 // Kernel selection: the one-warp DMMA kernel (hsw_dmma1.cu) for every shape it
 // instantiates (2D Q2/Q3, 3D Q2-Q4: all five configs); the W-warps-per-pair DMMA
 // kernel (hsw_dmma.cu) for the other orders.  HSW_KERNEL=dmma forces the latter.
+// HSW_D2=1|0 forces the two-warp kernel (hsw_dmma2.cu) on / off where it is instantiated.
 int kernel_choice_for(int dim, int p) {
     static const bool force_dmma = [] {
         const char* k = std::getenv("HSW_KERNEL");
         return k && std::string(k) == "dmma";
     }();
+    static const int d2 = [] {
+        const char* e = std::getenv("HSW_D2");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (!force_dmma && d2 == 1 && dev_dmma2_supported(dim, p)) return 4;
     return (!force_dmma && dev_dmma1_supported(dim, p)) ? 3 : 2;
 }
 
 void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
-    if (kernel_choice_for(h->S.dim, h->S.p) == 3)
+    const int kc = kernel_choice_for(h->S.dim, h->S.p);
+    if (kc == 4)
+        dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+    else if (kc == 3)
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
     else
         dev_dmma_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
@@ -1779,7 +1788,7 @@ bool dataflow_enabled(const hsw_handle* h) {
         const char* e = std::getenv("HSW_DATAFLOW");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    if (kernel_choice_for(h->S.dim, h->S.p) != 3) return false;
+    if (kernel_choice_for(h->S.dim, h->S.p) < 3) return false;
     return env >= 0 ? env == 1 : h->S.dim == 3;
 }
 
@@ -1801,8 +1810,12 @@ unsigned next_epoch(hsw_handle* h) {
 void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
     const unsigned ep = next_epoch(h);
     CUDA_OK(cudaMemsetAsync(h->d_done + (size_t)h->S.nel * h->S.nd + 1, 0, sizeof(unsigned), h->stream));
-    dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
-                    h->d_done, ep);
+    if (kernel_choice_for(h->S.dim, h->S.p) == 4)
+        dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
+                        h->d_done, ep);
+    else
+        dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
+                        h->d_done, ep);
 }
 
 // The all-ordinate sweep is one launch per level (C2: 449 levels of ~24 us):
@@ -2319,7 +2332,9 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
         CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         const int pr = e * h->S.nd + d;
         CUDA_OK(cudaMemcpyAsync(h->d_pair1, &pr, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-        if (kernel_choice_for(h->S.dim, h->S.p) == 3)
+        if (kernel_choice_for(h->S.dim, h->S.p) == 4)
+            dev_dmma2_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
+        else if (kernel_choice_for(h->S.dim, h->S.p) == 3)
             dev_dmma1_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);
         else
             dev_dmma_local_solve(h->P, h->d_pair1, h->d_vec, h->d_vec2, h->d_err, h->zero_pair, h->stream);

@@ -144,5 +144,12 @@ void dev_dmma1_sweep(const DevProblem& P, const double* src, const double* psi_o
                      unsigned* done_flags = nullptr, unsigned epoch = 0);
 void dev_dmma1_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                            unsigned long long* err_key, int64_t zero_pair, void* stream);
+// two warps per pair (hsw_dmma2.cu): the latency-bound 3D Q4 shape
+bool dev_dmma2_supported(int dim, int p);
+void dev_dmma2_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
+                     const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream,
+                     unsigned* done_flags = nullptr, unsigned epoch = 0);
+void dev_dmma2_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
+                           unsigned long long* err_key, int64_t zero_pair, void* stream);
 
 }  // namespace hsw

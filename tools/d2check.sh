@@ -1,0 +1,7 @@
+set -u
+o=gpurun_out/${1:-d2}
+mkdir -p $o
+export HSW_D2=1
+timeout 600 python -m pytest -q -x -p no:cacheprovider tests/test_gpu_parity.py -m gpu -k "c5 or single_hex or local_solve or singular" > $o/tests.log 2>&1; echo "rc=$?" >> $o/tests.log
+timeout 600 python tools/quick_bench.py c5 > $o/qb.log 2>&1; echo "rc=$?" >> $o/qb.log
+HSW_D2=0 timeout 600 python tools/quick_bench.py c5 >> $o/qb.log 2>&1
