@@ -55,13 +55,14 @@ struct D2 {
     static constexpr int RB = NL + NT;                  // register tile-columns [RB, NTC)
     static constexpr int NRW = (NTC - RB) / 2;          // register tile-columns per warp
     static_assert((NTC - RB) % 2 == 0 && NRW >= 1, "register tile-columns split evenly over the two warps");
-    static_assert(NL % 2 == 0 && NT % 2 == 0, "shared-memory and TMEM tile-columns split evenly (role = column parity)");
+    static_assert(NT % 2 == 0, "TMEM tile-columns split evenly over the two warps (role = column parity)");
     static constexpr int TCR = N / 8, QR = (N % 8) / 2, SR = N % 2;   // rhs tile-column / quad column / slot
     static constexpr int RHS_ROLE = TCR & 1;
-    static constexpr int JR = (TCR - NL_ - NT_ - RHS_ROLE) / 2;   // register slot of the rhs column in its owner
+    static constexpr int JR = (TCR - NL_ - NT_ - ((RHS_ROLE - NL_ - NT_) & 1)) / 2;   // register slot of the rhs column
     static_assert(TCR >= RB, "the rhs tile-column must be register resident");
     static constexpr int PAIRS = PAIRS_;
     static_assert(PAIRS % 4 == 0, "a pair's two warps must share a TMEM lane quarter");
+    static_assert(1 + 3 * PAIRS <= 16, "three named barriers per pair (ids 1..15)");
     static constexpr int WARPS = 2 * PAIRS;
     static constexpr int THREADS = 32 * WARPS;
     static constexpr int PPQ = PAIRS / 4;               // pairs per TMEM lane quarter
@@ -79,10 +80,10 @@ struct D2 {
     static constexpr int SM_WQ = SM_X;                                // [NF][NQF] signed (Omega.n) w|J|
     static constexpr int SM_UP = SM_WQ + NF * NQF;                    // [NF][NFN] upwind values / projections
     static constexpr int SM_TR = SM_UP + NF * NFN;                    // [NF][NQF] inflow traces * weight
-    static constexpr int SM_T1 = SM_TR + NF * NQF;                    // [T1SZ]
+    static constexpr int SM_T1 = SM_TR + NF * NQF;                    // [2 roles][T1SZ]
     static constexpr int FMS = NFN + 1;
-    static constexpr int SM_F = SM_T1 + T1SZ;                         // [NFN][FMS]
-    static constexpr int FACE_END = SM_F + NFN * FMS;
+    static constexpr int SM_F = SM_T1 + 2 * T1SZ;                     // [2 face parities][NFN][FMS]
+    static constexpr int FACE_END = SM_F + 2 * NFN * FMS;
     static constexpr int LPS = NR + (4 - NR % 16 + 16) % 16;           // = 4 (mod 16)
     static constexpr int NOWN = (NT + 1) / 2 + NRW;                   // TMEM + register tile-columns of a warp (max)
     static constexpr int URS = 8 * NOWN + (4 - (8 * NOWN) % 16 + 16) % 16;
@@ -161,8 +162,8 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     const int role = warp / G::PAIRS;          // 0 or 1: owns the tile-columns c with (c & 1) == role
     const int ps = warp % G::PAIRS;            // pair slot of the CTA
     const bool rhs_owner = role == G::RHS_ROLE;
-    // named barrier ids of this pair: 1 + 3 ps + {0: pair start / faces done (both sync);
-    // 1, 2: face block ready / consumed, then panel parity 0 / 1 (one arrives, one syncs)}
+    // named barrier ids of this pair: 1 + 3 ps + {0: pair start, each outflow face block, faces
+    // done (both sync); 1, 2: panel parity 0 / 1 (the producer arrives, the other syncs)}
     const int bid = 1 + 3 * ps;
     if (NT > 0) {
         if (warp == 0) {
@@ -242,9 +243,9 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     int* s_claim = reinterpret_cast<int*>(psm + G::SM_PAIR - 1);
     // own tile-columns: storage index of column c of this role
     // TMEM: tt = c - NL; own TMEM columns c = NL + t0 + 2 i, t0 = (NL ^ role) & 1 parity fix
-    // NL, NT even: role w owns SMEM columns w, w + 2, ..., TMEM columns tt = w, w + 2, ...
-    // (column NL + tt) and register columns RB + w + 2 j
-    const int t0 = role, l0 = role, r0 = role;
+    // role w owns the columns of parity w: SMEM columns w, w + 2, ...; TMEM columns NL + tt,
+    // tt = t0, t0 + 2, ...; register columns RB + r0 + 2 j
+    const int l0 = role, t0 = (role - NL) & 1, r0 = (role - RB) & 1;
     constexpr int NTOWN = NT / 2;
     auto owner_of = [](int c) { return c & 1; };
     unsigned* claim = done_flags ? done_flags + (size_t)pr.nel * pr.nd + 1 : nullptr;
@@ -329,16 +330,26 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         }
                     tm_put4(tt, grp, v);
                 };
-                // loads two groups ahead (few warps per SM: latency-bound)
                 constexpr int NGR = NTOWN * GPC;
-                double4 bq[3][4][2];
                 auto gi_tt = [&](int gi) { return t0 + 2 * (gi / GPC); };
-                if (NGR > 0) ldgrp(gi_tt(0), 0 % GPC, bq[0]);
-                if (NGR > 1) ldgrp(gi_tt(1), 1 % GPC, bq[1]);
+                if (G::PAIRS >= 8) {
+                    // many warps, 128 registers: one group in flight
+#pragma unroll 1
+                    for (int gi = 0; gi < NGR; ++gi) {
+                        double4 b[4][2];
+                        ldgrp(gi_tt(gi), gi % GPC, b);
+                        combine(gi_tt(gi), gi % GPC, b);
+                    }
+                } else {
+                    // few warps per SM (latency-bound): loads two groups ahead
+                    double4 bq[3][4][2];
+                    if (NGR > 0) ldgrp(gi_tt(0), 0 % GPC, bq[0]);
+                    if (NGR > 1) ldgrp(gi_tt(1), 1 % GPC, bq[1]);
 #pragma unroll
-                for (int gi = 0; gi < NGR; ++gi) {
-                    if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, bq[(gi + 2) % 3]);
-                    combine(gi_tt(gi), gi % GPC, bq[gi % 3]);
+                    for (int gi = 0; gi < NGR; ++gi) {
+                        if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, bq[(gi + 2) % 3]);
+                        combine(gi_tt(gi), gi % GPC, bq[gi % 3]);
+                    }
                 }
             }
 #pragma unroll
@@ -465,16 +476,17 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     }
                 }
             }
-            // outflow blocks: role 0 forms each face's block, both warps add it to their own
-            // tile-columns (bid + 1: block ready, role 0 arrives; bid + 2: block consumed,
-            // role 1 arrives except after the last face)
+            // outflow blocks: both warps form half of each face's block (double-buffered by
+            // face parity; the first stage T1 privately), one barrier, then each adds it to
+            // its own tile-columns
             const int nout = __popc(outm);
             int om = outm;
             for (int k = 0; k < nout; ++k) {
                 const int f = __ffs(om) - 1;
                 om &= om - 1;
-                if (role == 0) {
-                    if (k > 0) pbar_sync(bid + 2);
+                double* T1w = T1 + role * G::T1SZ;
+                double* FMk = FM + (k & 1) * NFN * G::FMS;
+                {
                     for (int idx = lane; idx < NQ1 * NS1; idx += 32) {
                         const int jq = idx / NS1;
                         const int tri = s_tri1[idx - jq * NS1];
@@ -482,25 +494,22 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         double t = 0.0;
 #pragma unroll
                         for (int iq = 0; iq < NQ1; ++iq) t += fmax(WQ[f * NQF + jq * NQ1 + iq], 0.0) * s_l2[(iq * N1 + aa) * N1 + ab];
-                        T1[(jq * N1 + aa) * N1 + ab] = t;
-                        T1[(jq * N1 + ab) * N1 + aa] = t;
+                        T1w[(jq * N1 + aa) * N1 + ab] = t;
+                        T1w[(jq * N1 + ab) * N1 + aa] = t;
                     }
                     __syncwarp();
-                    for (int idx = lane; idx < NSF; idx += 32) {
+                    for (int idx = 2 * lane + role; idx < NSF; idx += 64) {
                         const int tri = s_tri[idx];
                         const int fa = tri & 255, fb = tri >> 8;
                         const int a0 = fa % N1, b0 = fa / N1, a1 = fb % N1, b1 = fb / N1;
                         double t = 0.0;
 #pragma unroll
-                        for (int jq = 0; jq < NQ1; ++jq) t += T1[(jq * N1 + a0) * N1 + a1] * s_l2[(jq * N1 + b0) * N1 + b1];
-                        FM[fa * G::FMS + fb] = t;
-                        FM[fb * G::FMS + fa] = t;
+                        for (int jq = 0; jq < NQ1; ++jq) t += T1w[(jq * N1 + a0) * N1 + a1] * s_l2[(jq * N1 + b0) * N1 + b1];
+                        FMk[fa * G::FMS + fb] = t;
+                        FMk[fb * G::FMS + fa] = t;
                     }
-                    pbar_arrive(bid + 1);
-                    __syncwarp();
-                } else {
-                    pbar_sync(bid + 1);
                 }
+                pbar_sync(bid);   // the block is complete (and the other warp is past face k - 1)
                 int rf[NTR];
 #pragma unroll
                 for (int tr = 0; tr < NTR; ++tr) {
@@ -516,7 +525,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         if (__any_sync(FULL, cf >= 0)) {
 #pragma unroll
                             for (int tr = 0; tr < NTR; ++tr)
-                                if (cf >= 0 && rf[tr] >= 0) acc[j][tr][s] += FM[rf[tr] + cf];
+                                if (cf >= 0 && rf[tr] >= 0) acc[j][tr][s] += FMk[rf[tr] + cf];
                         }
                     }
                 for (int tl = l0; tl < NL; tl += 2)
@@ -526,7 +535,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         if (__any_sync(FULL, cf >= 0)) {
 #pragma unroll
                             for (int tr = 0; tr < NTR; ++tr)
-                                if (cf >= 0 && rf[tr] >= 0) AL[((tl * NTR + tr) * 32 + lsw) * 2 + s] += FM[rf[tr] + cf];
+                                if (cf >= 0 && rf[tr] >= 0) AL[((tl * NTR + tr) * 32 + lsw) * 2 + s] += FMk[rf[tr] + cf];
                         }
                     }
                 for (int tt = t0; tt < NT; tt += 2) {
@@ -540,15 +549,14 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk) {
                                 const int rr = rf[4 * grp + kk];
-                                if (rr >= 0 && cf0 >= 0) v[kk][0] += FM[rr + cf0];
-                                if (rr >= 0 && cf1 >= 0) v[kk][1] += FM[rr + cf1];
+                                if (rr >= 0 && cf0 >= 0) v[kk][0] += FMk[rr + cf0];
+                                if (rr >= 0 && cf1 >= 0) v[kk][1] += FMk[rr + cf1];
                             }
                             tm_put4(tt, grp, v);
                         }
                     }
                 }
                 __syncwarp();
-                if (role == 1 && k + 1 < nout) pbar_arrive(bid + 2);
             }
         }
         if ((int64_t)pair == zero_pair) {   // test hook: zero the (e, d) block (own columns)
@@ -580,6 +588,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         bool singular = false;
         // factor panel Pn (its tile-column is own): partial pivoting in row layout; publish
         // L~ = L L11^{-1} into Lp[Pn & 1], the pivot rows into s_pst[Pn & 1], the steps
+        bool pan_ready = false;   // the next panel (a TMEM column) is already in the panel buffer
         auto factor = [&](int Pn) {
             const int TCp = (Pn * PW) >> 3, h = ((Pn * PW) >> 2) & 1;
             double* Lp = psm + G::SM_LP + (Pn % G::NLP) * G::LPB;
@@ -606,7 +615,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
             } else {
                 const bool wr = (q >> 1) == h;
                 const int js = q - 2 * h;
-                if (TCp < RB) {
+                if (TCp < RB && !pan_ready) {
 #pragma unroll
                     for (int grp = 0; grp < NTR / 4; ++grp) {
                         double v[4][2];
@@ -763,7 +772,9 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         };
         // update of an own TMEM tile-column c: its pivot rows (one x4 load per row, the
         // holders write UR), then the software-pipelined tile pass
-        auto upd_tmem = [&](int c) __attribute__((always_inline)) {
+        auto upd_tmem = [&](int c, double* pan, int h) __attribute__((always_inline)) {
+            // pan != nullptr: this is the next panel's column; its half h is also written to the
+            // panel buffer in row layout (the factorization then skips its TMEM reload)
             const int tt = c - NL;
             const int us = (tt - t0) >> 1;
             tm_wait_st();
@@ -799,9 +810,17 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
 #pragma unroll
                 for (int k = 0; k < 4; ++k) mma884(v[k][0], v[k][1], af[4 * grp + k], b);
                 tm_put4(tt, grp, v);
+                if (pan) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int r = 8 * (4 * grp + k) + g;
+                        st_shared_v2_if(pan + r * PW + 2 * ((q - 2 * h) ^ ((r >> 2) & 1)), v[k][0], v[k][1],
+                                        (q >> 1) == h);
+                    }
+                }
                 if (grp + 1 < GPC) tm_wait_ld();
             }
-            __syncwarp();   // UR reuse
+            __syncwarp();   // UR reuse (and the panel written)
         };
         // update of own REGISTER tile-column j (column RB + role + 2 j)
         auto upd_reg = [&](int j) __attribute__((always_inline)) {
@@ -827,6 +846,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
             // first live column) and factors Pn + 1 before its other updates
             const bool la = Pn + 1 < NPANEL && owner(panel_col(Pn + 1)) == role;
             int c = G::NTC;   // first own live column not yet updated
+            pan_ready = false;
             if (Pn >= 0) {
                 if (owner(panel_col(Pn)) != role) pbar_sync(bid + 1 + (Pn & 1));   // published by the other warp
                 const double* Lp = psm + G::SM_LP + (Pn % G::NLP) * G::LPB;
@@ -849,9 +869,14 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                 const int tcn = min(((Pn + 1) * PW) >> 3, TCR);   // first live column (= the next panel's)
                 c = tcn + ((tcn & 1) != role);
                 if (la) {   // the next panel's column
-                    if (c < NL) upd_smem(c);
-                    else if (c < RB) upd_tmem(c);
-                    else upd_reg((c - RB - role) >> 1);
+                    if (c < NL) {
+                        upd_smem(c);
+                    } else if (c < RB) {
+                        upd_tmem(c, psm + G::SM_LP + ((Pn + 1) % G::NLP) * G::LPB, (((Pn + 1) * PW) >> 2) & 1);
+                        pan_ready = true;
+                    } else {
+                        upd_reg((c - RB - r0) >> 1);
+                    }
                     c += 2;
                 }
             }
@@ -863,10 +888,10 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
 #pragma unroll 1
             for (; c < NL; c += 2) upd_smem(c);
 #pragma unroll 1
-            for (; c < RB; c += 2) upd_tmem(c);
+            for (; c < RB; c += 2) upd_tmem(c, nullptr, 0);
 #pragma unroll
             for (int j = 0; j < NRW; ++j)
-                if (RB + role + 2 * j >= c) upd_reg(j);
+                if (RB + r0 + 2 * j >= c) upd_reg(j);
         }
 
         // ------------------------------------------------ solution x_k = rhs(p_k) * (1 / pivot_k)
@@ -928,7 +953,8 @@ void launch_dmma2(const DevProblem& pr, const double* src, const double* psi_old
 
 }  // namespace
 
-// HSW_D2=1 selects the two-warp kernel for the shapes it instantiates (3D p = 4)
+// The two-warp kernel's shape: 3D p = 4 (C5).  Measured for 3D p = 3 (C4) too, with four
+// two-warp pairs per SM: 544 ms vs the one-warp kernel's 319 ms (twelve pairs per SM).
 bool dev_dmma2_supported(int dim, int p) { return dim == 3 && p == 4; }
 
 void dev_dmma2_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
@@ -938,6 +964,7 @@ void dev_dmma2_sweep(const DevProblem& P, const double* src, const double* psi_o
     if (P.dim == 3 && P.p == 4)
         launch_dmma2<4, 4, 8, 4>(P, src, psi_old, psi_new, psi_new, stride, pairs, npairs, nullptr, err_key, zero_pair,
                                  st, done_flags, epoch);
+
     else
         throw Error(-1, "dmma2 kernel: unsupported (dim, order)");
 }
@@ -948,6 +975,7 @@ void dev_dmma2_local_solve(const DevProblem& P, const int* pair_dev, const doubl
     if (P.dim == 3 && P.p == 4)
         launch_dmma2<4, 4, 8, 4>(P, nullptr, nullptr, nullptr, out, 0, pair_dev, 1, rhs, err_key, zero_pair, st,
                                  nullptr, 0);
+
     else
         throw Error(-1, "dmma2 kernel: unsupported (dim, order)");
 }
