@@ -753,7 +753,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         auto panel_col = [](int Pn) { return (Pn * PW) >> 3; };
         (void)owner;
         // Per-panel state of the update (registers): L~ fragments, pivot rows, row steps
-        double af[NTR];
+        const double* afp = nullptr;   // this panel's L~ fragments: afp[8 tr] (read where used: fewer live registers)
         int pstv[PW], tsv[NTR];
         int pq = -1;
         // update of an own SHARED-MEMORY tile-column c with the current panel
@@ -765,7 +765,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
 #pragma unroll
             for (int tr = 0; tr < NTR; ++tr) {
                 double2 cc = *reinterpret_cast<const double2*>(base + tr * 64);
-                mma884(cc.x, cc.y, af[tr], b);
+                mma884(cc.x, cc.y, afp[8 * tr], b);
                 *reinterpret_cast<double2*>(base + tr * 64) = cc;
             }
             __syncwarp();
@@ -808,7 +808,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     v[k][1] = u2d(cur[4 * k + 2], cur[4 * k + 3]);
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) mma884(v[k][0], v[k][1], af[4 * grp + k], b);
+                for (int k = 0; k < 4; ++k) mma884(v[k][0], v[k][1], afp[8 * (4 * grp + k)], b);
                 tm_put4(tt, grp, v);
                 if (pan) {
 #pragma unroll
@@ -835,7 +835,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     __syncwarp();
                     const double b = pq >= 0 ? UR[q * G::URS + 8 * us + g] : 0.0;
 #pragma unroll
-                    for (int tr = 0; tr < NTR; ++tr) mma884(acc[jj][tr][0], acc[jj][tr][1], af[tr], b);
+                    for (int tr = 0; tr < NTR; ++tr) mma884(acc[jj][tr][0], acc[jj][tr][1], afp[8 * tr], b);
                     __syncwarp();
                 }
         };
@@ -850,8 +850,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
             if (Pn >= 0) {
                 if (owner(panel_col(Pn)) != role) pbar_sync(bid + 1 + (Pn & 1));   // published by the other warp
                 const double* Lp = psm + G::SM_LP + (Pn % G::NLP) * G::LPB;
-#pragma unroll
-                for (int tr = 0; tr < NTR; ++tr) af[tr] = Lp[q * G::LPS + 8 * tr + g];
+                afp = Lp + q * G::LPS + g;
 #pragma unroll
                 for (int t = 0; t < PW; ++t) pstv[t] = s_pst[(Pn % G::NLP) * PW + t];
                 if (owner(panel_col(Pn)) != role) {   // the other warp retired these rows

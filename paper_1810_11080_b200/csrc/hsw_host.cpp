@@ -525,56 +525,6 @@ struct Mesh {
 // ------------------------------------------------------------ sweep graph
 struct Edge { int from, to; double weight; };
 
-// sweepgraph.hpp:82-136
-static std::vector<std::vector<int>> tarjan_scc(int n, const std::vector<Edge>& edges) {
-    std::vector<std::vector<int>> adj(n);
-    for (size_t i = 0; i < edges.size(); ++i) adj[edges[i].from].push_back((int)i);
-    std::vector<int> index(n, -1), low(n, 0), stack;
-    std::vector<char> on(n, 0);
-    std::vector<std::vector<int>> sccs;
-    int next = 0;
-    struct Frame { int v; size_t child; };
-    std::vector<Frame> call;
-    for (int root = 0; root < n; ++root) {
-        if (index[root] != -1) continue;
-        call.push_back({root, 0});
-        index[root] = low[root] = next++;
-        stack.push_back(root);
-        on[root] = 1;
-        while (!call.empty()) {
-            Frame& fr = call.back();
-            if (fr.child < adj[fr.v].size()) {
-                const int w = edges[adj[fr.v][fr.child++]].to;
-                if (index[w] == -1) {
-                    index[w] = low[w] = next++;
-                    stack.push_back(w);
-                    on[w] = 1;
-                    call.push_back({w, 0});
-                } else if (on[w]) {
-                    low[fr.v] = std::min(low[fr.v], index[w]);
-                }
-            } else {
-                if (low[fr.v] == index[fr.v]) {
-                    std::vector<int> comp;
-                    int w;
-                    do {
-                        w = stack.back();
-                        stack.pop_back();
-                        on[w] = 0;
-                        comp.push_back(w);
-                    } while (w != fr.v);
-                    std::sort(comp.begin(), comp.end());
-                    sccs.push_back(std::move(comp));
-                }
-                const int v = fr.v;
-                call.pop_back();
-                if (!call.empty()) low[call.back().v] = std::min(low[call.back().v], low[v]);
-            }
-        }
-    }
-    return sccs;
-}
-
 struct Fas { std::vector<int> order, lagged; double weight = 0.0; };
 struct Local { std::vector<int> verts; std::vector<std::array<int, 2>> e; std::vector<double> w; std::vector<int> parent; };
 
@@ -723,51 +673,105 @@ struct Ordering {
     double lagged_weight = 0.0;
 };
 
-// sweepgraph.hpp:331-396
+// Tarjan (sweepgraph.hpp:82-136) over the CSR adjacency, flat outputs: the same visit
+// order (roots ascending, out-edges by ascending edge id) as tarjan_scc, so the same
+// components in the same emission order, each sorted ascending; no per-vertex vectors.
+struct FlatScc { std::vector<int> comp, off, verts; };
+static FlatScc tarjan_flat(int n, const OutCsr& g, const std::vector<Edge>& edges) {
+    FlatScc r;
+    r.comp.assign(n, -1);
+    r.off.push_back(0);
+    r.verts.reserve(n);
+    std::vector<int> index(n, -1), low(n, 0), stack;
+    std::vector<char> on(n, 0);
+    struct Frame { int v, child; };
+    std::vector<Frame> call;
+    int next = 0;
+    for (int root = 0; root < n; ++root) {
+        if (index[root] != -1) continue;
+        call.push_back({root, g.off[root]});
+        index[root] = low[root] = next++;
+        stack.push_back(root);
+        on[root] = 1;
+        while (!call.empty()) {
+            Frame& fr = call.back();
+            if (fr.child < g.off[fr.v + 1]) {
+                const int w = edges[g.eid[fr.child++]].to;
+                if (index[w] == -1) {
+                    index[w] = low[w] = next++;
+                    stack.push_back(w);
+                    on[w] = 1;
+                    call.push_back({w, g.off[w]});
+                } else if (on[w]) {
+                    low[fr.v] = std::min(low[fr.v], index[w]);
+                }
+            } else {
+                const int v = fr.v;
+                if (low[v] == index[v]) {
+                    const size_t b = r.verts.size();
+                    int w;
+                    do {
+                        w = stack.back();
+                        stack.pop_back();
+                        on[w] = 0;
+                        r.verts.push_back(w);
+                    } while (w != v);
+                    std::sort(r.verts.begin() + b, r.verts.end());
+                    const int c = (int)r.off.size() - 1;
+                    for (size_t k = b; k < r.verts.size(); ++k) r.comp[r.verts[k]] = c;
+                    r.off.push_back((int)r.verts.size());
+                }
+                call.pop_back();
+                if (!call.empty()) low[call.back().v] = std::min(low[call.back().v], low[v]);
+            }
+        }
+    }
+    return r;
+}
+
+// sweepgraph.hpp:331-396 (flat-array restatement; same order, cut set and weights)
 static Ordering sweep_ordering(int n, const std::vector<Edge>& edges, int thr) {
-    const auto sccs = tarjan_scc(n, edges);
-    std::vector<int> comp(n, -1);
-    for (size_t c = 0; c < sccs.size(); ++c)
-        for (int v : sccs[c]) comp[v] = (int)c;
-    const int nc = (int)sccs.size();
-    std::vector<std::vector<int>> cout_(nc);
-    std::vector<int> cin(nc, 0);
+    const OutCsr g = out_csr(n, edges);
+    const FlatScc S = tarjan_flat(n, g, edges);
+    const std::vector<int>& comp = S.comp;
+    const int nc = (int)S.off.size() - 1;
+    // condensation edges, sorted unique per source component (CSR)
+    std::vector<std::pair<int, int>> ce;
     for (const auto& e : edges) {
         const int cu = comp[e.from], cv = comp[e.to];
-        if (cu != cv) cout_[cu].push_back(cv);
+        if (cu != cv) ce.push_back({cu, cv});
     }
-    for (int c = 0; c < nc; ++c) {
-        std::sort(cout_[c].begin(), cout_[c].end());
-        cout_[c].erase(std::unique(cout_[c].begin(), cout_[c].end()), cout_[c].end());
-        for (int t : cout_[c]) cin[t]++;
+    std::sort(ce.begin(), ce.end());
+    ce.erase(std::unique(ce.begin(), ce.end()), ce.end());
+    std::vector<int> coff((size_t)nc + 1, 0), cin(nc, 0);
+    for (const auto& pr : ce) {
+        coff[(size_t)pr.first + 1]++;
+        cin[pr.second]++;
     }
+    for (int c = 0; c < nc; ++c) coff[(size_t)c + 1] += coff[c];
     using Key = std::pair<int, int>;
     std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
     for (int c = 0; c < nc; ++c)
-        if (cin[c] == 0) ready.push({sccs[c].front(), c});
+        if (cin[c] == 0) ready.push({S.verts[S.off[c]], c});
     Ordering res;
     res.order.reserve(n);
-    std::vector<int> scratch, ks;
-    OutCsr g;
-    bool have_csr = false;
+    std::vector<int> scratch, ks, vs;
     while (!ready.empty()) {
         const int c = ready.top().second;
         ready.pop();
-        if (sccs[c].size() == 1) {
-            res.order.push_back(sccs[c].front());
+        const int sz = S.off[c + 1] - S.off[c];
+        if (sz == 1) {
+            res.order.push_back(S.verts[S.off[c]]);
         } else {
-            if (!have_csr) {
-                g = out_csr(n, edges);
-                have_csr = true;
-            }
-            const Local lg = induce_csr(g, edges, sccs[c], scratch, ks);
-            const Fas fas = (int)sccs[c].size() <= std::min(thr, 22) ? fas_exact(lg) : fas_heuristic(lg);
+            vs.assign(S.verts.begin() + S.off[c], S.verts.begin() + S.off[c + 1]);
+            const Local lg = induce_csr(g, edges, vs, scratch, ks);
+            const Fas fas = sz <= std::min(thr, 22) ? fas_exact(lg) : fas_heuristic(lg);
             res.order.insert(res.order.end(), fas.order.begin(), fas.order.end());
             res.lagged_edges.insert(res.lagged_edges.end(), fas.lagged.begin(), fas.lagged.end());
             res.lagged_weight += fas.weight;
         }
-        for (int t : cout_[c])
-            if (--cin[t] == 0) ready.push({sccs[t].front(), t});
+        for (int k = coff[c]; k < coff[(size_t)c + 1]; ++k)
+            if (--cin[ce[k].second] == 0) ready.push({S.verts[S.off[ce[k].second]], ce[k].second});
     }
     if ((int)res.order.size() != n) throw Error(HSW_ERR_LOGIC, "sweep_ordering: condensation was not acyclic");
     res.position.assign(n, -1);

@@ -18,3 +18,9 @@ for _ in range(reps):
     ms = L.hsw_last_sweep_kernel_ms(s.handle)
 pairs = P.num_elements * P.num_ordinates
 print(f"{name} cells={cells} dirs={P.num_ordinates} levels={s.num_levels} sweep {ms:.3f} ms {pairs/ms*1e3:.3e} solves/s")
+if os.environ.get("HSW_LEVEL_SIZES", "1") == "1":
+    import numpy as np
+    cnt = np.zeros(s.num_levels, np.int64)
+    for d in range(P.num_ordinates):
+        cnt += np.bincount(s.ordering(d).level, minlength=s.num_levels)[: s.num_levels]
+    print("level_sizes", " ".join(str(int(x)) for x in cnt))
