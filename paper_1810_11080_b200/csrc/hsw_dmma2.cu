@@ -138,6 +138,38 @@ __device__ __forceinline__ void st_shared_v2_if(double* p, double x, double y, b
                  ::"r"((uint32_t)__cvta_generic_to_shared(p)), "d"(x), "d"(y), "r"((int)on) : "memory");
 }
 __device__ __forceinline__ double u2d(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+// 4 tile fragments (8 doubles) of TMEM: load + wait + pairing in ONE asm statement, so the
+// compiler sees doubles (no register moves re-pairing the b32 halves, no pins after the wait)
+__device__ __forceinline__ void tm_ld16w(uint32_t a, double (&v)[8]) {
+    asm volatile("{\n .reg .b32 t<16>;\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x16.b32 {t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15}, [%8];\n"
+                 " tcgen05.wait::ld.sync.aligned;\n"
+                 " mov.b64 %0, {t0,t1};\n mov.b64 %1, {t2,t3};\n mov.b64 %2, {t4,t5};\n mov.b64 %3, {t6,t7};\n"
+                 " mov.b64 %4, {t8,t9};\n mov.b64 %5, {t10,t11};\n mov.b64 %6, {t12,t13};\n mov.b64 %7, {t14,t15};\n}"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+                 : "r"(a) : "memory");
+}
+__device__ __forceinline__ void tm_st16w(uint32_t a, const double (&v)[8]) {
+    asm volatile("{\n .reg .b32 t<16>;\n"
+                 " mov.b64 {t0,t1}, %1;\n mov.b64 {t2,t3}, %2;\n mov.b64 {t4,t5}, %3;\n mov.b64 {t6,t7}, %4;\n"
+                 " mov.b64 {t8,t9}, %5;\n mov.b64 {t10,t11}, %6;\n mov.b64 {t12,t13}, %7;\n mov.b64 {t14,t15}, %8;\n"
+                 " tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {t0,t1,t2,t3,t4,t5,t6,t7,t8,t9,t10,t11,t12,t13,t14,t15};\n}"
+                 ::"r"(a), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "d"(v[4]), "d"(v[5]), "d"(v[6]), "d"(v[7])
+                 : "memory");
+}
+// one x4 fragment (2 doubles) from each of 4 TMEM column addresses, one wait
+__device__ __forceinline__ void tm_ld4x4w(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, double (&v)[8]) {
+    asm volatile("{\n .reg .b32 t<16>;\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t0,t1,t2,t3}, [%8];\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t4,t5,t6,t7}, [%9];\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t8,t9,t10,t11}, [%10];\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x4.b32 {t12,t13,t14,t15}, [%11];\n"
+                 " tcgen05.wait::ld.sync.aligned;\n"
+                 " mov.b64 %0, {t0,t1};\n mov.b64 %1, {t2,t3};\n mov.b64 %2, {t4,t5};\n mov.b64 %3, {t6,t7};\n"
+                 " mov.b64 %4, {t8,t9};\n mov.b64 %5, {t10,t11};\n mov.b64 %6, {t12,t13};\n mov.b64 %7, {t14,t15};\n}"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3) : "memory");
+}
 // named barriers of a pair (64 threads: its two warps)
 __device__ __forceinline__ void pbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void pbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
@@ -205,27 +237,11 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     // the pair's TMEM: lane quarter ps % 4, column range (ps / 4) * TCOLS
     const uint32_t tmw = NT > 0 ? s_tmem_base + ((uint32_t)(32 * (ps & 3)) << 16) + (uint32_t)((ps >> 2) * G::TCOLS) : 0u;
     auto tm_get4 = [&](int tt, int grp, double (&v)[4][2]) {
-        uint32_t r[16];
         tm_wait_st();
-        tm_ld16(tmw + (uint32_t)((tt * NTR + 4 * grp) * 4), r);
-        tm_wait_ld();
-        tm_pin(r);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            v[k][0] = u2d(r[4 * k], r[4 * k + 1]);
-            v[k][1] = u2d(r[4 * k + 2], r[4 * k + 3]);
-        }
+        tm_ld16w(tmw + (uint32_t)((tt * NTR + 4 * grp) * 4), *reinterpret_cast<double (*)[8]>(&v[0][0]));
     };
     auto tm_put4 = [&](int tt, int grp, const double (&v)[4][2]) {
-        uint32_t r[16];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            r[4 * k] = (uint32_t)__double2loint(v[k][0]);
-            r[4 * k + 1] = (uint32_t)__double2hiint(v[k][0]);
-            r[4 * k + 2] = (uint32_t)__double2loint(v[k][1]);
-            r[4 * k + 3] = (uint32_t)__double2hiint(v[k][1]);
-        }
-        tm_st16(tmw + (uint32_t)((tt * NTR + 4 * grp) * 4), r);
+        tm_st16w(tmw + (uint32_t)((tt * NTR + 4 * grp) * 4), *reinterpret_cast<const double (*)[8]>(&v[0][0]));
     };
 
     double* psm = smem + G::TAB_TOTAL + (size_t)ps * G::SM_PAIR;
@@ -341,14 +357,16 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         combine(gi_tt(gi), gi % GPC, b);
                     }
                 } else {
-                    // few warps per SM (latency-bound): loads two groups ahead
-                    double4 bq[3][4][2];
-                    if (NGR > 0) ldgrp(gi_tt(0), 0 % GPC, bq[0]);
-                    if (NGR > 1) ldgrp(gi_tt(1), 1 % GPC, bq[1]);
-#pragma unroll
-                    for (int gi = 0; gi < NGR; ++gi) {
-                        if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, bq[(gi + 2) % 3]);
-                        combine(gi_tt(gi), gi % GPC, bq[gi % 3]);
+                    // loads one group ahead, two groups per (rolled) iteration: a small code
+                    // footprint (eight warps per SM share the instruction cache)
+                    double4 b0[4][2], b1[4][2];
+                    ldgrp(gi_tt(0), 0, b0);
+#pragma unroll 1
+                    for (int gi = 0; gi < NGR; gi += 2) {
+                        if (gi + 1 < NGR) ldgrp(gi_tt(gi + 1), (gi + 1) % GPC, b1);
+                        combine(gi_tt(gi), gi % GPC, b0);
+                        if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, b0);
+                        if (gi + 1 < NGR) combine(gi_tt(gi + 1), (gi + 1) % GPC, b1);
                     }
                 }
             }
@@ -778,35 +796,23 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
             const int tt = c - NL;
             const int us = (tt - t0) >> 1;
             tm_wait_st();
-            uint32_t rv[PW][4];
+            {
+                auto pa = [&](int t) { return tmw + (uint32_t)((tt * NTR + ((pstv[t] >= 0 ? pstv[t] : 0) >> 3)) * 4); };
+                double rv[8];
+                tm_ld4x4w(pa(0), pa(1), pa(2), pa(3), rv);
 #pragma unroll
-            for (int t = 0; t < PW; ++t)
-                tm_ld4(tmw + (uint32_t)((tt * NTR + ((pstv[t] >= 0 ? pstv[t] : 0) >> 3)) * 4), rv[t]);
-            tm_wait_ld();
-#pragma unroll
-            for (int t = 0; t < PW; ++t) {
-                tm_pin(rv[t]);
-                const int p = pstv[t] >= 0 ? pstv[t] : 0;
-                st_shared_v2_if(UR + t * G::URS + 2 * q + 8 * us, u2d(rv[t][0], rv[t][1]), u2d(rv[t][2], rv[t][3]),
-                                pstv[t] >= 0 && g == (p & 7));
+                for (int t = 0; t < PW; ++t) {
+                    const int p = pstv[t] >= 0 ? pstv[t] : 0;
+                    st_shared_v2_if(UR + t * G::URS + 2 * q + 8 * us, rv[2 * t], rv[2 * t + 1], pstv[t] >= 0 && g == (p & 7));
+                }
             }
             __syncwarp();
             const double b = pq >= 0 ? UR[q * G::URS + 8 * us + g] : 0.0;
             constexpr int GPC = NTR / 4;
-            uint32_t rbuf[2][16];
-            tm_ld16(tmw + (uint32_t)((tt * NTR) * 4), rbuf[0]);
-            tm_wait_ld();
 #pragma unroll
             for (int grp = 0; grp < GPC; ++grp) {
-                uint32_t (&cur)[16] = rbuf[grp & 1];
-                tm_pin(cur);
-                if (grp + 1 < GPC) tm_ld16(tmw + (uint32_t)((tt * NTR + 4 * (grp + 1)) * 4), rbuf[(grp + 1) & 1]);
                 double v[4][2];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    v[k][0] = u2d(cur[4 * k], cur[4 * k + 1]);
-                    v[k][1] = u2d(cur[4 * k + 2], cur[4 * k + 3]);
-                }
+                tm_ld16w(tmw + (uint32_t)((tt * NTR + 4 * grp) * 4), *reinterpret_cast<double (*)[8]>(&v[0][0]));
 #pragma unroll
                 for (int k = 0; k < 4; ++k) mma884(v[k][0], v[k][1], afp[8 * (4 * grp + k)], b);
                 tm_put4(tt, grp, v);
@@ -818,7 +824,6 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                                         (q >> 1) == h);
                     }
                 }
-                if (grp + 1 < GPC) tm_wait_ld();
             }
             __syncwarp();   // UR reuse (and the panel written)
         };
