@@ -468,7 +468,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     double t = pr.inflow;
                     if ((inm >> f) & 1) {
                         t = 0.0;
-#pragma unroll
+#pragma unroll 5
                         for (int aa = 0; aa < NFN; ++aa) t += s_trace[qq * G::TRS + aa] * UP[f * NFN + aa];
                     }
                     TR[sl * NQF + qq] = t * fmax(-WQ[f * NQF + qq], 0.0);
@@ -477,20 +477,21 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                 for (int idx = lane; idx < nin * NFN; idx += 32) {
                     const int sl = idx / NFN, a = idx - sl * NFN;
                     double t = 0.0;
-#pragma unroll
+#pragma unroll 6
                     for (int qq = 0; qq < NQF; ++qq) t += TR[sl * NQF + qq] * s_trace[qq * G::TRS + a];
                     UP[idx] = t;
                 }
                 __syncwarp();
-                if (infm) {
+                if (infm && q == QR) {   // the rhs lanes: a short data-dependent loop per row
 #pragma unroll
                     for (int tr = 0; tr < NTR; ++tr) {
                         const int r = 8 * tr + g;
-                        const int m = (q == QR && r < N) ? s_nmask[r] & infm : 0;
-#pragma unroll
-                        for (int f = 0; f < NF; ++f)
-                            if ((m >> f) & 1)
-                                acc[G::JR][tr][SR] += UP[__popc(infm & ((1 << f) - 1)) * NFN + s_fidx[f * N + r]];
+                        int m = r < N ? s_nmask[r] & infm : 0;
+                        while (m) {
+                            const int f = __ffs(m) - 1;
+                            m &= m - 1;
+                            acc[G::JR][tr][SR] += UP[__popc(infm & ((1 << f) - 1)) * NFN + s_fidx[f * N + r]];
+                        }
                     }
                 }
             }
