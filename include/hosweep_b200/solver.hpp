@@ -9,6 +9,7 @@
 
 #include "hosweep_b200.h"
 
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -198,5 +199,49 @@ class SweepSolver {
     mutable std::vector<std::unique_ptr<SweepOrdering>> orderings_;
     std::unique_ptr<std::once_flag[]> ordering_once_;
 };
+
+// solver.hpp:209-245 balance_report: conservation functionals of a state
+struct BalanceReport {
+    double source_volume = 0.0, inflow = 0.0, source_total = 0.0, absorption = 0.0, outflow = 0.0,
+           net_leakage = 0.0, residual = 0.0;
+    std::map<int, double> outflow_by_attr;   // keyed by boundary attribute
+};
+
+namespace detail {
+inline BalanceReport balance_from(const double out5[5], const int* attrs, const double* vals, int n) {
+    BalanceReport r;
+    r.source_volume = out5[0];
+    r.inflow = out5[1];
+    r.source_total = out5[0] + out5[1];
+    r.absorption = out5[2];
+    r.outflow = out5[3];
+    r.net_leakage = out5[3] - out5[1];
+    r.residual = out5[4];
+    for (int i = 0; i < n; ++i) r.outflow_by_attr[attrs[i]] = vals[i];
+    return r;
+}
+}  // namespace detail
+
+// balance_report(op, state) for a state held on the host
+inline BalanceReport balance_report(const SweepSolver& s, const SolverState& st) {
+    const size_t N = (size_t)s.num_dofs();
+    std::vector<double> psi(N * (size_t)s.num_ordinates());
+    for (int d = 0; d < s.num_ordinates(); ++d) std::copy(st.psi[d].begin(), st.psi[d].end(), psi.begin() + d * N);
+    double out5[5];
+    int attrs[64], cnt = 0;
+    double vals[64];
+    check(hsw_balance(s.handle(), psi.data(), st.phi.data(), out5, attrs, vals, 64, &cnt));
+    return detail::balance_from(out5, attrs, vals, cnt < 64 ? cnt : 64);
+}
+
+// balance_report of the solver's converged state while it is still on the device
+// (after source_iteration(); no host round trip of psi)
+inline BalanceReport balance_report_resident(const SweepSolver& s) {
+    double out5[5];
+    int attrs[64], cnt = 0;
+    double vals[64];
+    check(hsw_balance_resident(s.handle(), out5, attrs, vals, 64, &cnt));
+    return detail::balance_from(out5, attrs, vals, cnt < 64 ? cnt : 64);
+}
 
 }  // namespace hosweep_b200

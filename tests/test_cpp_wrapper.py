@@ -10,6 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SRC = r'''
 #include "hosweep_b200/solver.hpp"
+#include <cmath>
 #include <cstdio>
 #include <vector>
 int main() {
@@ -33,6 +34,14 @@ int main() {
     try { s.ordering(1); return 4; } catch (const std::out_of_range&) {}
     try { s.sweep(0, std::vector<double>(8), std::vector<double>(8)); return 5; }
     catch (const hosweep_b200::DeviceError&) {}
+    // balance_report (solver.hpp:220-245) of a host state: psi = phi = 1, Omega = +x ->
+    // outflow only through the x = 2 face (attribute 2), its length times 4 pi
+    hosweep_b200::SolverState stt;
+    stt.psi.assign(1, std::vector<double>(8, 1.0));
+    stt.phi.assign(8, 1.0);
+    const auto br = hosweep_b200::balance_report(s, stt);
+    if (br.outflow_by_attr.size() != 4 || std::abs(br.outflow - 12.566370614359172) > 1e-12 ||
+        std::abs(br.outflow_by_attr.at(2) - br.outflow) > 1e-12) return 7;
     d.num_boundary_faces = 5;  // face left undeclared -> MeshError (mesh.hpp:333-337)
     try { hosweep_b200::SweepSolver bad(d); return 6; } catch (const hosweep_b200::MeshError&) {}
     std::puts("cpp wrapper ok");

@@ -22,14 +22,24 @@ ref = json.loads(last_json(f"{o}/bench_ref.log"))
 open(f"{P}/{tag}_bench_c4.json", "w").write(json.dumps(bench) + "\n")
 open(f"{P}/{tag}_bench_reference_c4.json", "w").write(json.dumps(ref) + "\n")
 
-cfg = open(f"{o}/configs.md").read().strip()
-open(f"{P}/{tag}_configs.md", "w").write(
-    f"# {tag} per-config report (B200, one GPU): per-sweep throughput and time to converge\n\n"
-    "`python tools/report_configs.py` — each BASELINE.json config at full size: one all-ordinate sweep "
-    "(device-resident, CUDA events, best of 3; one dataflow launch of the one-warp DMMA kernel per 3D sweep, "
-    "per-level launches of the same kernel from a CUDA graph for 2D), then source iteration from psi = 0, "
-    "phi = 0 to ||dphi||_2 / ||phi||_2 < 1e-8 (`hsw_source_iteration`, device time incl. the phi reductions).\n\n"
-    + cfg + "\n\nTFLOP/s = F(n) pairs / sweep time, F(n) = 2/3 n^3 + 2 n^2 (LU-algorithmic, SURVEY §8d).\n")
+pc = bench.get("per_config") or {}
+CL = [f"# {tag} per-config report (B200, one GPU, measured inside the bench run)", "",
+      "`bench.py`'s `per_config` block: each BASELINE.json config at full size, one all-ordinate sweep "
+      "(device-resident, CUDA events on the library stream, best of 3 after 2 warm-ups), then source iteration "
+      "from psi = phi = 0 to ||dphi||_2 / ||phi||_2 < 1e-8 (`hsw_source_iteration`, device time).", "",
+      "| config | pairs | n | sweep ms | solves/s | TFLOP/s (LU-alg) | roofline frac | SI iterations | SI s | setup s |",
+      "|---|---|---|---|---|---|---|---|---|---|"]
+for name in ("c1", "c2", "c3", "c4", "c5"):
+    r = pc.get(name, {})
+    if "sweep_ms" in r:
+        CL.append(f"| {name} | {r['pairs']:,} | {r['n']} | {r['sweep_ms']:.2f} | {r['solves_per_s']:.4g} | "
+                  f"{r['tflops_lu_alg']:.2f} | {r['roofline_frac']:.4f} | {r['si_iterations']} | {r['si_s']:.2f} | "
+                  f"{r['setup_s']:.2f} |")
+    else:
+        CL.append(f"| {name} | error: {r.get('error')} |")
+CL += ["", "TFLOP/s = F(n) pairs / sweep time, F(n) = 2/3 n^3 + 2 n^2 (LU-algorithmic, SURVEY §8d); roofline "
+       f"frac against the in-run measured FP64 peak ({bench['roofline']['peak']:.2f} TFLOP/s)."]
+open(f"{P}/{tag}_configs.md", "w").write("\n".join(CL) + "\n")
 
 rows = [r for r in csv.reader(open(f"{o}/launches.csv")) if r]
 i0 = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -72,46 +82,66 @@ json.dump({"dram_bytes_per_sweep": rd + wr,
                    "tensor per (level, element): 2.36 M visits = 309 GB) + psi; bench.py reports it per launch"},
           open(f"{P}/traffic_c4.json", "w"), indent=1)
 
-raw = list(csv.reader(open(f"{o}/raw.csv")))
-d = dict(zip(raw[0], raw[2]))
-sys.argv = ["x", f"{o}/src.csv", obj, KSUB]
-srcl = open(os.path.join(ROOT, "paper_1810_11080_b200/csrc/hsw_dmma1.cu")).read().splitlines()
-g = {"__name__": "x", "sys": sys}
-exec(open(os.path.join(ROOT, "tools/ncu_lines.py")).read().split("ts = sum")[0], g)
-lagg, stl = g["agg"], g["stl"]
-T = sum(v[0] for v in lagg.values())
-E = sum(v[1] for v in lagg.values())
-npair = 42792
-M = [f"# {tag}: C4 sweep kernel profile", "",
-     f"Bench (profiles/{tag}_bench_c4.json): {bench['ms_per_step']:.1f} ms per sweep, {bench['value'] / 1e6:.2f} M solves/s, "
-     f"{bench['roofline']['achieved']:.2f} TFLOP/s LU-algorithmic = {100 * bench['roofline']['frac']:.1f} % of the "
-     f"{bench['roofline']['peak']:.2f} TFLOP/s measured FP64 peak; e2e {bench['e2e']['value'] / 1e6:.2f} M solves/s.", "",
-     "## Whole-sweep DRAM traffic", "",
+
+
+def ncu_section(sub, cfg, src_file, obj_file, ksub, label):
+    """Markdown of one --set full capture under gpurun_out/TAG/SUB (tools/ncu_case.sh)."""
+    od = f"{o}/{sub}"
+    raw = list(csv.reader(open(f"{od}/raw.csv")))
+    d = dict(zip(raw[0], raw[2]))
+    log = open(f"{od}/ncu_full.log").read()
+    sizes = [int(x) for x in re.search(r"level_sizes (.*)", log).group(1).split()]
+    skip = {"c4": 300, "c5": 200}[cfg]
+    lvl = skip - len(sizes)
+    npair = sizes[lvl]
+    sys.argv = ["x", f"{od}/src.csv", obj_file, ksub]
+    srcl = open(os.path.join(ROOT, "paper_1810_11080_b200/csrc", src_file)).read().splitlines()
+    g = {"__name__": "x", "sys": sys}
+    exec(open(os.path.join(ROOT, "tools/ncu_lines.py")).read().split("ts = sum")[0], g)
+    lagg, stl = g["agg"], g["stl"]
+    T = sum(v[0] for v in lagg.values())
+    E = sum(v[1] for v in lagg.values())
+    M = [f"## {label}: one level, `--set full` (HSW_DATAFLOW=0, level {lvl}: {npair:,} pairs)", "",
+         "| metric | value |", "|---|---|"]
+    for k, lab in [("gpu__time_duration.sum", "duration (cold, serialised) ms"),
+                   ("launch__registers_per_thread", "registers"), ("launch__block_size", "threads per CTA"),
+                   ("launch__shared_mem_per_block_dynamic", "dynamic shared memory KB"),
+                   ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+                   ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+                   ("sm__inst_executed.avg.per_cycle_active", "IPC"),
+                   ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor (DMMA) pipe %"),
+                   ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
+                   ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1TEX throughput %"),
+                   ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
+                   ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank conflicts")]:
+        M.append(f"| {lab} | {d.get(k)} |")
+    M.append(f"| executed warp-instructions per pair | {E / npair:.0f} |")
+    st = {n: float(v.replace(",", "") or 0) for n, v in d.items()
+          if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio")}
+    M.append("| stalls per issue | " + ", ".join(f"{n.split('stalled_')[1].split('_per_issue')[0]} {v:.2f}"
+                                                 for n, v in sorted(st.items(), key=lambda x: -x[1])[:6]) + " |")
+    M += ["", "Top stall lines (SASS mapped to source with tools/ncu_lines.py):", "",
+          "| line | stall samples | executed | dominant stalls | source |", "|---|---|---|---|---|"]
+    for (fn, ln), (sm, e) in sorted(lagg.items(), key=lambda x: -x[1][0])[:12]:
+        why = " ".join(f"{k}:{v * 100 // max(sm, 1)}" for k, v in stl[(fn, ln)].most_common(2))
+        txt = srcl[ln - 1].strip()[:70].replace("|", "/") if fn == src_file else fn
+        M.append(f"| {ln} | {100 * sm / T:.1f} % | {100 * e / E:.1f} % | {why} | `{txt}` |")
+    return M
+
+
+r = bench["roofline"]
+M = [f"# {tag}: sweep kernel profiles (C4: hsw_dmma1, one warp per pair; C5: hsw_dmma2, two warps per pair)", "",
+     f"Bench (profiles/{tag}_bench_c4.json): C4 {bench['ms_per_step']:.1f} ms per sweep, {bench['value'] / 1e6:.2f} M "
+     f"solves/s, {r['achieved']:.2f} TFLOP/s LU-algorithmic = {100 * r['frac']:.1f} % of the {r['peak']:.2f} TFLOP/s "
+     f"measured FP64 peak; e2e {bench['e2e']['value'] / 1e6:.2f} M solves/s.", "",
+     "## C4 whole-sweep DRAM traffic", "",
      f"Single dataflow launch (one full C4 sweep) under ncu: {tr['gpu__time_duration.sum'] / 1e6:.1f} ms, DRAM read "
      f"{rd / 1e9:.1f} GB + write {wr / 1e9:.1f} GB = {(rd + wr) / PAIRS / 1e3:.1f} KB per pair "
      f"({(rd + wr) / (tr['gpu__time_duration.sum'] * 1e-9) / 1e12:.2f} TB/s average); L1 hit "
-     f"{tr['l1tex__t_sector_hit_rate.pct']:.1f} %, L2 hit {tr['lts__t_sector_hit_rate.pct']:.1f} %.", "",
-     "## One level, `--set full` (HSW_DATAFLOW=0, level 116: 42,792 pairs)", "", "| metric | value |", "|---|---|"]
-for k, label in [("gpu__time_duration.sum", "duration (cold, serialised) ms"), ("launch__registers_per_thread", "registers"),
-                 ("launch__shared_mem_per_block_dynamic", "dynamic shared memory KB"),
-                 ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
-                 ("sm__inst_executed.avg.per_cycle_active", "IPC"),
-                 ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor (DMMA) pipe %"),
-                 ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
-                 ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1TEX throughput %"),
-                 ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
-                 ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank conflicts")]:
-    M.append(f"| {label} | {d.get(k)} |")
-M.append(f"| executed warp-instructions per pair | {E / npair:.0f} |")
-st = {n: float(v.replace(",", "") or 0) for n, v in d.items()
-      if n.startswith("smsp__average_warps_issue_stalled") and n.endswith("per_issue_active.ratio")}
-M.append("| stalls per issue | " + ", ".join(f"{n.split('stalled_')[1].split('_per_issue')[0]} {v:.2f}"
-                                             for n, v in sorted(st.items(), key=lambda x: -x[1])[:6]) + " |")
-M += ["", "Top stall lines (SASS mapped to source with tools/ncu_lines.py):", "",
-      "| line | stall samples | executed | dominant stalls | source |", "|---|---|---|---|---|"]
-for (fn, ln), (s, e) in sorted(lagg.items(), key=lambda x: -x[1][0])[:12]:
-    why = " ".join(f"{k}:{v * 100 // max(s, 1)}" for k, v in stl[(fn, ln)].most_common(2))
-    txt = srcl[ln - 1].strip()[:70].replace("|", "/") if fn == "hsw_dmma1.cu" else fn
-    M.append(f"| {ln} | {100 * s / T:.1f} % | {100 * e / E:.1f} % | {why} | `{txt}` |")
-open(f"{P}/{tag}_ncu_c4.md", "w").write("\n".join(M) + "\n")
+     f"{tr['l1tex__t_sector_hit_rate.pct']:.1f} %, L2 hit {tr['lts__t_sector_hit_rate.pct']:.1f} %.", ""]
+M += ncu_section("c4", "c4", "hsw_dmma1.cu", obj, KSUB, "C4 (hsw_dmma1)")
+M += [""]
+M += ncu_section("c5", "c5", "hsw_dmma2.cu", obj.replace("hsw_dmma1", "hsw_dmma2"), "dmma2_sweep_kernelILi4ELi4ELi8ELi4E",
+                 "C5 (hsw_dmma2)")
+open(f"{P}/{tag}_ncu.md", "w").write("\n".join(M) + "\n")
 print("wrote", tag, "profiles")
