@@ -208,7 +208,11 @@ def run_ours(args):
 
     prob = pb.config(args.config)
     t0 = time.time()
-    solver = pk.SweepSolver(prob, device=local)
+    shard = None
+    if world > 1:   # a rank builds and holds only its ordinate block (plans, worklists, psi)
+        from paper_1810_11080_b200.sharded import block_of as _block_of
+        shard = _block_of(prob.num_ordinates, rank, world)
+    solver = pk.SweepSolver(prob, device=local, ordinate_range=shard)
     setup_s = time.time() - t0
     h = solver.handle
     pairs = prob.num_elements * prob.num_ordinates

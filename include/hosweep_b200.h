@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HSW_ABI_VERSION 3
+#define HSW_ABI_VERSION 4
 
 enum hsw_status {
     HSW_OK = 0,
@@ -103,6 +103,12 @@ typedef struct hsw_problem_desc {
     double romberg_tol;         /* default 1e-10 when <= 0                               */
     int romberg_max_levels;     /* default 16 when <= 0                                  */
     int romberg_min_levels;     /* default 6 when < 0 (0 is a valid value)              */
+    /* Ordinate shard [ordinate_begin, ordinate_end) of a multi-GPU rank:
+       only these ordinates' graphs, orders, worklists and psi are built / allocated;
+       the hsw_shard_* primitives, hsw_sweep_resident and single-ordinate calls inside
+       the shard work, all-ordinate calls (source_iteration, balance, d = -1 sweeps)
+       report HSW_ERR_RANGE.  ordinate_end == 0: every ordinate.                      */
+    int ordinate_begin, ordinate_end;
 } hsw_problem_desc;
 enum hsw_face_rule { HSW_FACE_GAUSS = 0, HSW_FACE_ROMBERG = 1 };
 

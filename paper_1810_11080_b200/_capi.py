@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libhosweep_b200.so")
 
-HSW_ABI_VERSION = 3
+HSW_ABI_VERSION = 4
 HSW_OK = 0
 STATUS_NAMES = {
     -1: "HSW_ERR_INVALID", -2: "HSW_ERR_MESH", -3: "HSW_ERR_GEOMETRY", -4: "HSW_ERR_ASSEMBLY",
@@ -47,7 +47,7 @@ class hsw_problem_desc(C.Structure):
         ("weighting", C.c_int), ("exact_fas_threshold", C.c_int), ("validate_geometry", C.c_int),
         ("check_local_blocks", C.c_int), ("device", C.c_int),
         ("face_rule", C.c_int), ("romberg_tol", C.c_double), ("romberg_max_levels", C.c_int),
-        ("romberg_min_levels", C.c_int),
+        ("romberg_min_levels", C.c_int), ("ordinate_begin", C.c_int), ("ordinate_end", C.c_int),
     ]
 
 

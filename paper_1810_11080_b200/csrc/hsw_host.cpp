@@ -896,6 +896,9 @@ struct Setup {
     double source_params[8] = {0};
     double inflow = 0.0;
     int vol_pts = 0, face_pts = 0, weighting = 1, fas_thr = 10;
+    // ordinate shard [ob, oe) of this handle (all ordinates unless a multi-GPU rank's block)
+    int ob = 0, oe = 0;
+    bool partial() const { return ob != 0 || oe != nd; }
     // FaceIntegration (assembly.hpp:33-40): Gauss (face_pts) or Romberg (2D)
     int face_rule = HSW_FACE_GAUSS;
     double rom_tol = 1e-10;
@@ -1001,6 +1004,15 @@ struct Setup {
         face_pts = D->face_points > 0 ? D->face_points : p + 2;
         weighting = D->weighting;
         fas_thr = D->exact_fas_threshold > 0 ? D->exact_fas_threshold : 10;
+        ob = 0;
+        oe = nd;
+        if (D->ordinate_end != 0) {
+            if (D->ordinate_begin < 0 || D->ordinate_end > nd || D->ordinate_begin >= D->ordinate_end)
+                throw Error(HSW_ERR_RANGE, "hsw_create: ordinate shard [" + std::to_string(D->ordinate_begin) + ", " +
+                                               std::to_string(D->ordinate_end) + ") out of range");
+            ob = D->ordinate_begin;
+            oe = D->ordinate_end;
+        }
         face_rule = D->face_rule;
         if (face_rule != HSW_FACE_GAUSS && face_rule != HSW_FACE_ROMBERG)
             throw Error(HSW_ERR_INVALID, "hsw_create: unknown face rule");
@@ -1292,8 +1304,8 @@ struct Setup {
             rom_omask.assign((size_t)nd * nel, 0);
             rom_unconverged.assign(nd, 0);
         }
-        parallel_for(nd, [&](int64_t d64) {
-            const int d = (int)d64;
+        parallel_for(oe - ob, [&](int64_t i64) {
+            const int d = ob + (int)i64;
             const double* om = &odir[3 * d];
             std::vector<double> LR((size_t)nfn * nfn), RL((size_t)nfn * nfn), wp(nqf), wm(nqf);
             auto& cpl = couplings[d];
@@ -1399,7 +1411,8 @@ struct Setup {
                     double length = 0.0;
                     for (int q = 0; q < nqf; ++q) length += fq_w[q] * sjv[q];
                     const double eps = 1e-12 * length;
-                    const double mlr = dev_cmax[((size_t)d * nfi + fi) * 2], mrl = dev_cmax[((size_t)d * nfi + fi) * 2 + 1];
+                    const double mlr = dev_cmax[((size_t)(d - ob) * nfi + fi) * 2],
+                                 mrl = dev_cmax[((size_t)(d - ob) * nfi + fi) * 2 + 1];
                     if (mlr > eps) {
                         cpl.push_back({fi, F.el, F.er, F.fl, F.fr});
                         wts.push_back(weight_of(mlr, F.el, F.fl, LR, false));
@@ -1530,25 +1543,25 @@ struct Setup {
         return w;
     }
 
-    void worklists() {
+    void worklists() {   // over the handle's ordinate shard [ob, oe)
         int maxl = 0;
-        for (int d = 0; d < nd; ++d)
+        for (int d = ob; d < oe; ++d)
             for (int e = 0; e < nel; ++e) maxl = std::max(maxl, ords[d].level[e]);
         num_levels = maxl + 1;
-        // all-ordinate worklist sorted by (level, element, ordinate)
+        // shard worklist sorted by (level, element, ordinate)
         std::vector<int> count(num_levels + 1, 0);
         for (int e = 0; e < nel; ++e)
-            for (int d = 0; d < nd; ++d) count[ords[d].level[e] + 1]++;
+            for (int d = ob; d < oe; ++d) count[ords[d].level[e] + 1]++;
         for (int l = 0; l < num_levels; ++l) count[l + 1] += count[l];
         level_offsets = count;
-        pairs_all.assign((size_t)nel * nd, 0);
+        pairs_all.assign((size_t)nel * (oe - ob), 0);
         std::vector<int> fill(count.begin(), count.end() - 1);
         for (int e = 0; e < nel; ++e)
-            for (int d = 0; d < nd; ++d) pairs_all[fill[ords[d].level[e]]++] = e * nd + d;
+            for (int d = ob; d < oe; ++d) pairs_all[fill[ords[d].level[e]]++] = e * nd + d;
         // per-ordinate worklists
         pairs_dir.assign((size_t)nel * nd, 0);
         dir_level_offsets.assign(nd, {});
-        for (int d = 0; d < nd; ++d) {
+        for (int d = ob; d < oe; ++d) {
             int ml = 0;
             for (int e = 0; e < nel; ++e) ml = std::max(ml, ords[d].level[e]);
             std::vector<int> c(ml + 2, 0);
@@ -1579,6 +1592,7 @@ struct hsw_handle {
     // device buffers
     double *d_rom_ob = nullptr, *d_rom_ib = nullptr, *d_rom_bin = nullptr;
     int* d_bfaces = nullptr;   // (elem, face, attr) per boundary face, for the device balance
+    size_t psi_offset = 0;     // d_psiA / d_psiB point psi_offset doubles before their allocations (shards)
     unsigned char* d_rom_omask = nullptr;
     double *d_T = nullptr, *d_sig_t = nullptr, *d_sig_s = nullptr, *d_qvol = nullptr, *d_fgeom = nullptr;
     double* d_bscale = nullptr;
@@ -1677,6 +1691,8 @@ T* dev_upload(const std::vector<T>& v) {
 
 void free_handle(hsw_handle* h) {
     if (!h) return;
+    if (h->d_psiA) h->d_psiA += h->psi_offset;
+    if (h->d_psiB) h->d_psiB += h->psi_offset;
     void* bufs[] = {h->d_T, h->d_sig_t, h->d_bscale, h->d_sig_s, h->d_qvol, h->d_fgeom, h->d_fnbr, h->d_inflags,
                     h->d_omega, h->d_weight, h->d_psiA, h->d_psiB, h->d_phi, h->d_phi_old, h->d_src,
                     h->d_scratch, h->d_out, h->d_vec, h->d_vec2, h->d_pairs_all, h->d_pairs_dir, h->d_pair1,
@@ -1702,6 +1718,21 @@ void free_handle(hsw_handle* h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
+}
+
+// shard handles (hsw_problem_desc::ordinate_begin/end): ordinates outside the shard and
+// calls that need every ordinate are range errors
+void need_in_shard(const hsw_handle* h, int d, const char* what) {
+    if (d >= 0 && (d < h->S.ob || d >= h->S.oe))
+        throw hsw::Error(HSW_ERR_RANGE, std::string(what) + ": ordinate " + std::to_string(d) +
+                                            " is not in this handle's shard [" + std::to_string(h->S.ob) + ", " +
+                                            std::to_string(h->S.oe) + ")");
+}
+void need_all_ordinates(const hsw_handle* h, const char* what) {
+    if (h->S.partial())
+        throw hsw::Error(HSW_ERR_RANGE, std::string(what) + ": needs every ordinate; this handle holds the shard [" +
+                                            std::to_string(h->S.ob) + ", " + std::to_string(h->S.oe) +
+                                            ") (use the hsw_shard_* primitives)");
 }
 
 void need_device(const hsw_handle* h) {
@@ -1830,7 +1861,7 @@ void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const
 void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool time_it) {
     if (time_it) CUDA_OK(cudaEventRecord(h->ev0, h->stream));
     if (dataflow_enabled(h)) {
-        dataflow_sweep(h, psi_old, psi_new, h->d_pairs_all, (int)((size_t)h->S.nel * h->S.nd));
+        dataflow_sweep(h, psi_old, psi_new, h->d_pairs_all, (int)h->S.pairs_all.size());
         h->last_launches = 1;
         if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
         return;
@@ -2034,7 +2065,7 @@ void device_init(hsw_handle* h, int device) {
 void device_coupling_max(hsw_handle* h) {
     Setup& S = h->S;
     const int nfi = (int)S.mesh.ifaces.size();
-    S.dev_cmax.assign((size_t)S.nd * nfi * 2, 0.0);
+    S.dev_cmax.assign((size_t)(S.oe - S.ob) * nfi * 2, 0.0);
     if (nfi == 0) return;
     std::vector<int> iface((size_t)nfi * 5);
     for (int i = 0; i < nfi; ++i) {
@@ -2054,12 +2085,12 @@ void device_coupling_max(hsw_handle* h) {
     const int chunk = std::max(1, std::min(S.nd, (int)(std::max<size_t>(1, (size_t)(256u << 20) / ((size_t)nfi * 16)))));
     double* d_out = nullptr;
     CUDA_OK(cudaMalloc(&d_out, (size_t)chunk * nfi * 2 * sizeof(double)));
-    for (int d0 = 0; d0 < S.nd; d0 += chunk) {
-        const int d1 = std::min(S.nd, d0 + chunk);
+    for (int d0 = S.ob; d0 < S.oe; d0 += chunk) {
+        const int d1 = std::min(S.oe, d0 + chunk);
         dev_coupling_max(S.dim, nfi, S.nf, S.nqf, S.nfn, d_if, d_geo, d_sj, d_w, d_tr, d_trR, d_od, d0, d1, d_out,
                          h->stream);
-        CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)d0 * nfi * 2], d_out, (size_t)(d1 - d0) * nfi * 2 * sizeof(double),
-                                cudaMemcpyDeviceToHost, h->stream));
+        CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)(d0 - S.ob) * nfi * 2], d_out,
+                                (size_t)(d1 - d0) * nfi * 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     }
     CUDA_OK(cudaStreamSynchronize(h->stream));
     for (void* b : {(void*)d_if, (void*)d_geo, (void*)d_sj, (void*)d_w, (void*)d_tr, (void*)d_trR, (void*)d_od,
@@ -2196,11 +2227,16 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         h->d_pairs_all = dev_upload(S.pairs_all);
         h->d_pairs_dir = dev_upload(S.pairs_dir);
         h->N = (size_t)S.nel * S.nb;
-        const size_t psi_bytes = h->N * S.nd * sizeof(double);
+        // psi of the shard's ordinates only; the handle's pointers are offset so that row d of
+        // the global [nd][N] layout addresses ordinate d (kernels index psi by global d)
+        const size_t psi_bytes = h->N * (size_t)(S.oe - S.ob) * sizeof(double);
         CUDA_OK(cudaMalloc(&h->d_psiA, psi_bytes));
         CUDA_OK(cudaMalloc(&h->d_psiB, psi_bytes));
         CUDA_OK(cudaMemset(h->d_psiA, 0, psi_bytes));
         CUDA_OK(cudaMemset(h->d_psiB, 0, psi_bytes));
+        h->psi_offset = (size_t)S.ob * h->N;
+        h->d_psiA -= h->psi_offset;
+        h->d_psiB -= h->psi_offset;
         CUDA_OK(cudaMalloc(&h->d_phi, h->N * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_phi_old, h->N * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_src, h->N * sizeof(double)));
@@ -2278,6 +2314,8 @@ int hsw_ordering(const hsw_handle* h, int d, int* order, int* position, int* lag
                  int* num_lagged, double* lagged_weight, int* level) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_ordering: null handle");
     if (d < 0 || d >= h->S.nd) return fail(HSW_ERR_RANGE, "vector::_M_range_check: ordinate " + std::to_string(d));
+    if (d < h->S.ob || d >= h->S.oe)
+        return fail(HSW_ERR_RANGE, "hsw_ordering: ordinate " + std::to_string(d) + " is not in this handle's shard");
     const Ordering& o = h->S.ords[d];
     if (order) std::copy(o.order.begin(), o.order.end(), order);
     if (position) std::copy(o.position.begin(), o.position.end(), position);
@@ -2299,6 +2337,8 @@ int hsw_total_lagged_edges(const hsw_handle* h, int64_t* out) {
 int hsw_couplings(const hsw_handle* h, int d, int* ints4, double* weights, int cap, int* count) {
     if (!h) return fail(HSW_ERR_INVALID, "hsw_couplings: null handle");
     if (d < 0 || d >= h->S.nd) return fail(HSW_ERR_RANGE, "hsw_couplings: ordinate out of range");
+    if (d < h->S.ob || d >= h->S.oe)
+        return fail(HSW_ERR_RANGE, "hsw_couplings: ordinate " + std::to_string(d) + " is not in this handle's shard");
     const auto& c = h->S.couplings[d];
     if (count) *count = (int)c.size();
     const int n = std::min<int>(cap, (int)c.size());
@@ -2333,6 +2373,7 @@ int hsw_local_solve(hsw_handle* h, int e, int d, const double* rhs, double* out)
         need_device(h);
         if (e < 0 || e >= h->S.nel || d < 0 || d >= h->S.nd)
             throw hsw::Error(HSW_ERR_RANGE, "hsw_local_solve: element/ordinate out of range");
+        need_in_shard(h, d, "hsw_local_solve");
         const size_t nb = h->S.nb;
         CUDA_OK(cudaMemcpyAsync(h->d_vec, rhs, nb * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         const int pr = e * h->S.nd + d;
@@ -2355,6 +2396,8 @@ int hsw_sweep_device(hsw_handle* h, int d, const double* phi_dev, const double* 
         HandleScope hs(h);
         need_device(h);
         if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
+        if (d == -1) need_all_ordinates(h, "hsw_sweep_device(d = -1)");
+        need_in_shard(h, d, "hsw_sweep_device");
         dev_scatter_source(h->P, phi_dev, h->d_src, h->stream);
         if (d == -1) {
             run_all_levels(h, psi_old_dev, psi_new_dev, false);
@@ -2556,6 +2599,8 @@ int hsw_sweep(hsw_handle* h, int d, const double* phi, const double* psi_old, do
         HandleScope hs(h);
         need_device(h);
         if (d < -1 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_sweep: ordinate out of range");
+        if (d == -1) need_all_ordinates(h, "hsw_sweep(d = -1)");
+        need_in_shard(h, d, "hsw_sweep");
         const size_t N = h->N;
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         if (d == -1) {
@@ -2579,6 +2624,7 @@ int hsw_direct_oracle(hsw_handle* h, int d, const double* phi, double* psi) {
         HandleScope hs(h);
         need_device(h);
         if (d < 0 || d >= h->S.nd) throw hsw::Error(HSW_ERR_RANGE, "hsw_direct_oracle: ordinate out of range");
+        need_in_shard(h, d, "hsw_direct_oracle");
         const size_t N = h->N;
         CUDA_OK(cudaMemcpyAsync(h->d_phi_old, phi, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         CUDA_OK(cudaMemsetAsync(h->d_vec, 0, N * sizeof(double), h->stream));
@@ -2596,6 +2642,7 @@ int hsw_source_iteration(hsw_handle* h, const hsw_si_options* opts, hsw_si_resul
         if (!h || !opts) throw hsw::Error(HSW_ERR_INVALID, "hsw_source_iteration: null argument");
         HandleScope hs(h);
         need_device(h);
+        need_all_ordinates(h, "hsw_source_iteration");
         const size_t N = h->N;
         const int nd = h->S.nd;
         CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
@@ -2668,6 +2715,7 @@ int hsw_balance(hsw_handle* h, const double* psi, const double* phi, double out5
     return guarded([&] {
         if (!h || !psi || !phi || !out5) throw hsw::Error(HSW_ERR_INVALID, "hsw_balance: null argument");
         HandleScope hs(h);
+        need_all_ordinates(h, "hsw_balance");
         const Setup& S = h->S;
         const size_t N = h->N;
         const int nfn = S.nfn, nqf = S.nqf, nb = S.nb;
@@ -2755,6 +2803,7 @@ int hsw_balance_resident(hsw_handle* h, double out5[5], int* attrs, double* vals
         if (!h || !out5) throw hsw::Error(HSW_ERR_INVALID, "hsw_balance_resident: null argument");
         HandleScope hs(h);
         need_device(h);
+        need_all_ordinates(h, "hsw_balance_resident");
         const Setup& S = h->S;
         const int nbf = (int)S.mesh.bfaces.size();
         if (!h->d_bfaces && nbf > 0) {
@@ -2818,7 +2867,8 @@ int hsw_set_state(hsw_handle* h, const double* phi, const double* psi) {
         need_device(h);
         if (phi) CUDA_OK(cudaMemcpyAsync(h->d_phi, phi, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
         if (psi)
-            CUDA_OK(cudaMemcpyAsync(h->d_psiA, psi, h->N * h->S.nd * sizeof(double), cudaMemcpyHostToDevice,
+            CUDA_OK(cudaMemcpyAsync(h->d_psiA + (size_t)h->S.ob * h->N, psi,
+                                    h->N * (size_t)(h->S.oe - h->S.ob) * sizeof(double), cudaMemcpyHostToDevice,
                                     h->stream));
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return HSW_OK;
@@ -2840,7 +2890,7 @@ int hsw_sweep_resident(hsw_handle* h) {
 // ---- direction-sharded source iteration primitives
 namespace {
 void check_block(const hsw_handle* h, int d0, int d1, const char* what) {
-    if (d0 < 0 || d1 > h->S.nd || d0 >= d1)
+    if (d0 < h->S.ob || d1 > h->S.oe || d0 >= d1)
         throw hsw::Error(HSW_ERR_RANGE, std::string(what) + ": ordinate block [" + std::to_string(d0) + ", " +
                                             std::to_string(d1) + ") out of range");
 }
@@ -2851,9 +2901,9 @@ int hsw_shard_reset(hsw_handle* h) {
         if (!h) throw hsw::Error(HSW_ERR_INVALID, "hsw_shard_reset: null handle");
         HandleScope hs(h);
         need_device(h);
-        const size_t N = h->N, nd = (size_t)h->S.nd;
-        CUDA_OK(cudaMemsetAsync(h->d_psiA, 0, N * nd * sizeof(double), h->stream));
-        CUDA_OK(cudaMemsetAsync(h->d_psiB, 0, N * nd * sizeof(double), h->stream));
+        const size_t N = h->N, ns = (size_t)(h->S.oe - h->S.ob), o = (size_t)h->S.ob * N;
+        CUDA_OK(cudaMemsetAsync(h->d_psiA + o, 0, N * ns * sizeof(double), h->stream));
+        CUDA_OK(cudaMemsetAsync(h->d_psiB + o, 0, N * ns * sizeof(double), h->stream));
         CUDA_OK(cudaMemsetAsync(h->d_phi, 0, N * sizeof(double), h->stream));
         return HSW_OK;
     });

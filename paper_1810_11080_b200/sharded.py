@@ -24,6 +24,9 @@ The exchange is an (N-1)-hop chain plus one broadcast of N_el*n doubles
 
 The driver talks to a *backend* (``DeviceShardBackend`` for the library; the
 CPU tests inject an oracle-backed one) so the collective logic is one code path.
+A rank creates its solver with ``SweepSolver(prob, device=local,
+ordinate_range=block_of(nd, rank, world))``: only its block's graphs, orders,
+worklists and psi are built (the element tensors are shared by all ordinates).
 """
 from __future__ import annotations
 

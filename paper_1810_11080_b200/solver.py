@@ -148,7 +148,11 @@ _WEIGHT = {"unity": 0, "face": 1, "siginvface": 2, "sig_inv_face": 2}
 
 class SweepSolver:
     def __init__(self, problem: Problem, options: Optional[SolveOptions] = None, device: int = 0,
-                 validate_geometry: bool = True, check_local_blocks: bool = True):
+                 validate_geometry: bool = True, check_local_blocks: bool = True,
+                 ordinate_range: Optional[Tuple[int, int]] = None):
+        """``ordinate_range=(d0, d1)``: a multi-GPU rank's shard — only those ordinates'
+        graphs, orders, worklists and psi are built (sharded.py); all-ordinate calls
+        (source_iteration, balance_report, sweep(-1)) then raise IndexError."""
         L = _capi.load()
         self.problem = problem
         self._options = options or SolveOptions()
@@ -192,6 +196,9 @@ class SweepSolver:
         d.romberg_tol = float(getattr(problem, "romberg_tol", 1e-10))
         d.romberg_max_levels = int(getattr(problem, "romberg_max_levels", 16))
         d.romberg_min_levels = int(getattr(problem, "romberg_min_levels", 6))
+        if ordinate_range is not None:
+            d.ordinate_begin, d.ordinate_end = int(ordinate_range[0]), int(ordinate_range[1])
+        self.ordinate_range = tuple(ordinate_range) if ordinate_range is not None else (0, problem.num_ordinates)
         h = C.c_void_p()
         _check(L.hsw_create(C.byref(d), C.byref(h)))
         self._h = h

@@ -149,3 +149,63 @@ def test_shard_sweep_host_matches_the_all_ordinate_sweep():
         assert np.array_equal(blk_new, ref[d0:d1]), (d0, d1)
         # launches summed over the pipelined sub-blocks: scatter + one dataflow launch each
         assert L.hsw_last_launch_count(s.handle) >= 2
+
+
+def test_shard_handle_plan_equals_the_full_plan():
+    """hsw_problem_desc::ordinate_begin/end (a rank's shard): the shard's orders / cut
+    sets equal the full handle's, other ordinates and all-ordinate calls are refused."""
+    import paper_1810_11080_b200 as pk
+    prob = pb.config("c3", cells=3, n_mu=2, n_az=4)
+    full = pk.SweepSolver(prob, device=-1)
+    part = pk.SweepSolver(prob, device=-1, ordinate_range=(2, 6))
+    assert part.ordinate_range == (2, 6)
+    for d in range(2, 6):
+        a, b = full.ordering(d), part.ordering(d)
+        assert (a.order == b.order).all() and (a.lagged_edges == b.lagged_edges).all() and (a.level == b.level).all()
+    assert part.total_lagged_edges() == sum(len(full.ordering(d).lagged_edges) for d in range(2, 6))
+    with pytest.raises(IndexError, match="shard"):
+        part.ordering(1)
+    with pytest.raises(IndexError):
+        pk.SweepSolver(prob, device=-1, ordinate_range=(5, 3))
+
+
+@pytest.mark.gpu
+def test_shard_handles_reproduce_the_full_handle_bit_for_bit():
+    """Two shard handles (what two ranks create) sweep their blocks and chain phi exactly
+    like one full handle's blocks: psi and phi identical bits for three iterations."""
+    import torch
+    import paper_1810_11080_b200 as pk
+    from paper_1810_11080_b200.sharded import DeviceShardBackend
+    prob = pb.config("c4", cells=6, n_mu=2, n_az=8)
+    nd = prob.num_ordinates
+    blocks = [(0, 7), (7, nd)]
+    full = DeviceShardBackend(pk.SweepSolver(prob))
+    parts = [DeviceShardBackend(pk.SweepSolver(prob, ordinate_range=b)) for b in blocks]
+    for be in [full] + parts:
+        be.reset()
+    phi_f = full.zeros()
+    phi_p = parts[0].zeros()
+    for it in range(3):
+        for (d0, d1) in blocks:
+            full.sweep(d0, d1, phi_f)
+        for be, (d0, d1) in zip(parts, blocks):
+            be.sweep(d0, d1, phi_p)
+        pf = None
+        for (d0, d1) in blocks:
+            out = full.zeros()
+            full.phi_partial(d0, d1, pf, out)
+            pf = out
+        pp = None
+        for be, (d0, d1) in zip(parts, blocks):
+            out = be.zeros()
+            be.phi_partial(d0, d1, pp, out)
+            pp = out
+        assert torch.equal(pf, pp), it
+        for be, (d0, d1) in zip(parts, blocks):
+            assert np.array_equal(be.psi(d0, d1), full.psi(d0, d1)), (it, d0)
+        full.advance(pf)
+        for be in parts:
+            be.advance(pp)
+        phi_f, phi_p = pf, pp
+    with pytest.raises(IndexError):
+        parts[0].solver.source_iteration()
