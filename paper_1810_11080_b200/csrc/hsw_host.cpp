@@ -1605,7 +1605,11 @@ struct hsw_handle {
     unsigned long long* d_prof = nullptr;
     int *d_tab_fnode = nullptr, *d_tab_fidx = nullptr, *d_tab_nmask = nullptr;
     double *d_tab_trace = nullptr, *d_tab_line = nullptr;
-    unsigned long long* d_err = nullptr;
+    unsigned long long* d_err = nullptr;   // [2]: singular block | static pivoting refused
+    // Static-pivot tile LU (the production sweep kernel) refused a block of this problem:
+    // every later sweep uses the pivoted Gauss-Jordan kernel (sticky)
+    bool need_pivot = false;
+    int64_t pivot_fallbacks = 0;
     double* h_out = nullptr;  // pinned
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t zero_pair = -1;
@@ -1741,6 +1745,10 @@ void need_device(const hsw_handle* h) {
                                        "the B200 sweep has no CPU fallback");
 }
 
+// Thrown by check_err when the static-pivot kernel refused a block: guarded() redoes the
+// API call once, now with the pivoted kernel (hsw_handle::need_pivot).
+struct RetryPivot {};
+
 // Raise the first singular (element, ordinate) recorded by the kernels.
 void check_err(hsw_handle* h) {
     if (h->d_done) {   // dataflow stall (see dmma1 kernel): results are invalid, fail loudly
@@ -1754,9 +1762,19 @@ void check_err(hsw_handle* h) {
                                            "(other work on the GPU?); set HSW_DATAFLOW=0");
         }
     }
-    unsigned long long key = 0;
-    CUDA_OK(cudaMemcpyAsync(&key, h->d_err, sizeof(key), cudaMemcpyDeviceToHost, h->stream));
+    unsigned long long keys[2] = {0, 0};
+    CUDA_OK(cudaMemcpyAsync(keys, h->d_err, sizeof(keys), cudaMemcpyDeviceToHost, h->stream));
     CUDA_OK(cudaStreamSynchronize(h->stream));
+    if (keys[1] != ~0ull) {
+        // the static-pivot kernel refused a block (tiny pivot or large inverse tile): its results
+        // are discarded, the handle switches to the pivoted kernel and the caller redoes the call
+        const unsigned long long reset[2] = {~0ull, ~0ull};
+        CUDA_OK(cudaMemcpy(h->d_err, reset, sizeof(reset), cudaMemcpyHostToDevice));
+        h->need_pivot = true;
+        ++h->pivot_fallbacks;
+        throw RetryPivot{};
+    }
+    const unsigned long long key = keys[0];
     if (key != ~0ull) {
         const int nd = h->S.nd;
         const long long pr = (long long)(key & 0xffffffffffull);
@@ -1786,9 +1804,32 @@ int kernel_choice_for(int dim, int p) {
     return (!force_dmma && dev_dmma1_supported(dim, p)) ? 3 : 2;
 }
 
-void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
+// Static-pivot tile LU (hsw_dmma1.cu, SP instantiations): the production sweep kernel
+// unless a block of this problem was refused (need_pivot) or HSW_SP=0.
+// HSW_SP_Q4=0/1 selects it for the 3D Q4 shape (else the two-warp pivoted kernel).
+bool static_pivot(const hsw_handle* h) {
+    static const int env = [] {
+        const char* e = std::getenv("HSW_SP");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    static const int q4 = [] {
+        const char* e = std::getenv("HSW_SP_Q4");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    if (env == 0 || h->need_pivot) return false;
     const int kc = kernel_choice_for(h->S.dim, h->S.p);
-    if (kc == 4)
+    if (kc == 4) return q4 == 1;
+    return kc == 3;
+}
+// 5: dmma1 static-pivot, 4: dmma2, 3: dmma1 pivoted, 2: dmma
+int kernel_choice(const hsw_handle* h) { return static_pivot(h) ? 5 : kernel_choice_for(h->S.dim, h->S.p); }
+
+void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
+    const int kc = kernel_choice(h);
+    if (kc == 5)
+        dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
+                        nullptr, 0, true);
+    else if (kc == 4)
         dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
     else if (kc == 3)
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
@@ -1824,7 +1865,7 @@ bool dataflow_enabled(const hsw_handle* h) {
         const char* e = std::getenv("HSW_DATAFLOW");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    if (kernel_choice_for(h->S.dim, h->S.p) < 3) return false;
+    if (kernel_choice(h) < 3) return false;
     return env >= 0 ? env == 1 : h->S.dim == 3;
 }
 
@@ -1846,12 +1887,13 @@ unsigned next_epoch(hsw_handle* h) {
 void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
     const unsigned ep = next_epoch(h);
     CUDA_OK(cudaMemsetAsync(h->d_done + (size_t)h->S.nel * h->S.nd + 1, 0, sizeof(unsigned), h->stream));
-    if (kernel_choice_for(h->S.dim, h->S.p) == 4)
+    const int kc = kernel_choice(h);
+    if (kc == 4)
         dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
                         h->d_done, ep);
     else
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
-                        h->d_done, ep);
+                        h->d_done, ep, kc == 5);
 }
 
 // The all-ordinate sweep is one launch per level (C2: 449 levels of ~24 us):
@@ -1866,7 +1908,7 @@ void run_all_levels(hsw_handle* h, const double* psi_old, double* psi_new, bool 
         if (time_it) CUDA_OK(cudaEventRecord(h->ev1, h->stream));
         return;
     }
-    const hsw_handle::GraphKey key{psi_old, psi_new, h->P.debug_flags, h->zero_pair, kernel_choice_for(h->S.dim, h->S.p)};
+    const hsw_handle::GraphKey key{psi_old, psi_new, h->P.debug_flags, h->zero_pair, kernel_choice(h)};
     auto it = h->graphs.find(key);
     if (!graphs_enabled() || (it == h->graphs.end() && !h->levels_configured)) {
         h->last_launches = launch_all_levels(h, psi_old, psi_new);
@@ -1991,7 +2033,14 @@ void run_dir_levels(hsw_handle* h, int d, const double* psi_old, double* psi_new
 template <typename F>
 int guarded(F&& f) {
     try {
-        return f();
+        try {
+            return f();
+        } catch (const RetryPivot&) {
+            // the static-pivot kernel refused a block: the handle now uses the pivoted kernel
+            return f();
+        }
+    } catch (const RetryPivot&) {
+        return fail(HSW_ERR_SOLVER, "static-pivot fallback raised twice");
     } catch (const hsw::Error& e) {
         return fail(e.status, e.what());
     } catch (const std::bad_alloc&) {
@@ -2246,11 +2295,11 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         CUDA_OK(cudaMemset(h->d_phi_old, 0, h->N * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_scratch, (size_t)3 * 65536 * sizeof(double)));
         CUDA_OK(cudaMalloc(&h->d_out, 8 * sizeof(double)));
-        CUDA_OK(cudaMalloc(&h->d_err, sizeof(unsigned long long)));
+        CUDA_OK(cudaMalloc(&h->d_err, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMalloc(&h->d_pair1, sizeof(int)));
         CUDA_OK(cudaMalloc(&h->d_prof, 16 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long)));
-        CUDA_OK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(h->d_err, 0xff, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMallocHost(&h->h_out, 8 * sizeof(double)));
         DevProblem& P = h->P;
         P.dim = S.dim; P.p = S.p; P.nb = S.nb; P.nfn = S.nfn; P.nqf = S.nqf; P.nfaces = S.nf;
@@ -2284,7 +2333,12 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             // SweepSolver ctor factor check (solver.hpp:67-75): one sweep on zero data
             dev_scatter_source(P, h->d_phi, h->d_src, h->stream);
             run_all_levels(h, h->d_psiA, h->d_psiB, false);
-            check_err(h);
+            try {
+                check_err(h);
+            } catch (const RetryPivot&) {   // decided here once: this problem needs row pivoting
+                run_all_levels(h, h->d_psiA, h->d_psiB, false);
+                check_err(h);
+            }
         }
         CUDA_OK(cudaStreamSynchronize(h->stream));
         return HSW_OK;

@@ -138,10 +138,14 @@ void dev_phi_norms2(const DevProblem& P, const double* phi_new, const double* ph
 // one warp per pair, persistent, register + shared-memory DMMA tiles (hsw_dmma1.cu)
 bool dev_dmma1_supported(int dim, int p);
 // done_flags != nullptr: dataflow schedule over the whole worklist (one launch;
-// a pair waits for its retained upwind pairs' flags == epoch, then publishes its own)
+// a pair waits for its retained upwind pairs' flags == epoch, then publishes its own).
+// static_pivot: the tile-LU instantiation without row searches; a pair whose block it
+// refuses (tiny pivot / large inverse tile) is recorded in err_key[1] (atomicMin of the
+// pair id) and the caller redoes the sweep with static_pivot = false.  err_key points
+// at TWO 64-bit keys: [0] singular block, [1] static pivoting refused.
 void dev_dmma1_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
                      const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream,
-                     unsigned* done_flags = nullptr, unsigned epoch = 0);
+                     unsigned* done_flags = nullptr, unsigned epoch = 0, bool static_pivot = false);
 void dev_dmma1_local_solve(const DevProblem& P, const int* pair_dev, const double* rhs, double* out,
                            unsigned long long* err_key, int64_t zero_pair, void* stream);
 // two warps per pair (hsw_dmma2.cu): the latency-bound 3D Q4 shape
