@@ -165,7 +165,7 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
     double acc[TCW][NTR][2];
     {
         const double st = pr.sig_t[e];
-        const double2* Te = reinterpret_cast<const double2*>(pr.T) + (size_t)e * N * N * 2;   // planar (t_idx)
+        const double2* Te = reinterpret_cast<const double2*>(pr.T) + (size_t)e * (t_elem_doubles(N) / 2);   // fragment order (t_idx)
 #pragma unroll
         for (int j = 0; j < TCW; ++j)
 #pragma unroll
@@ -176,8 +176,8 @@ dmma_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const dou
                     double v = 0.0;
                     if (r < N && c < N) {
                         const double4 t = (dbg & 4) ? make_double4(r == c ? 1.0 : 0.0, 0.0, 0.0, 0.0)
-                                                    : make_double4(Te[(size_t)(2 * c) * N + r].x, Te[(size_t)(2 * c) * N + r].y,
-                                                                  Te[(size_t)(2 * c + 1) * N + r].x, Te[(size_t)(2 * c + 1) * N + r].y);
+                                                    : make_double4(Te[t_idx2(N, r, c, 0)].x, Te[t_idx2(N, r, c, 0)].y, Te[t_idx2(N, r, c, 1)].x,
+                                                                  Te[t_idx2(N, r, c, 1)].y);
                         double gg = om0 * t.y + om1 * t.z;
                         if (DIM == 3) gg += om2 * t.w;
                         v = gg + st * t.x;

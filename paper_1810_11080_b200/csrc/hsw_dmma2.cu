@@ -289,7 +289,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         const double om0 = pr.omega[d * 4 + 0], om1 = pr.omega[d * 4 + 1], om2 = pr.omega[d * 4 + 2];
         const double amax = pr.bscale[e];
         if (role == 0 && !(pr.tune & 1)) {   // TMA L2 prefetch of the pair's element tensor
-            constexpr unsigned TB = (unsigned)(N * N * 4 * sizeof(double));
+            constexpr unsigned TB = (unsigned)(t_elem_doubles(N) * sizeof(double));
             constexpr unsigned CH = 32768u;
             const char* tb = reinterpret_cast<const char*>(pr.T) + (size_t)e * TB;
             if (lane < (int)((TB + CH - 1) / CH)) {
@@ -302,10 +302,10 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         double acc[NRW][NTR][2];
         {
             const double st = pr.sig_t[e];
-            const double2* Te = reinterpret_cast<const double2*>(pr.T) + (size_t)e * N * N * 2;
+            const double2* Te = reinterpret_cast<const double2*>(pr.T) + (size_t)e * (t_elem_doubles(N) / 2);
             const double* se = rhs_given ? rhs_given : src + (size_t)e * N;
             auto tload = [&](int r, int c) -> double4 {
-                const double2 a = __ldg(Te + (size_t)(2 * c) * N + r), b = __ldg(Te + (size_t)(2 * c + 1) * N + r);
+                const double2 a = __ldg(Te + t_idx2(N, r, c, 0)), b = __ldg(Te + t_idx2(N, r, c, 1));
                 return make_double4(a.x, a.y, b.x, b.y);
             };
             auto comb = [&](const double4 t) { return om0 * t.y + om1 * t.z + om2 * t.w + st * t.x; };

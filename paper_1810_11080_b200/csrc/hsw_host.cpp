@@ -2221,9 +2221,9 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             h->d_tab_line = dev_upload(line);
         }
         if (!S.T.empty()) {
-            // host tensors are [E][n][m][4]; the device layout is planar (t_idx)
+            // host tensors are [E][n][m][4]; the device layout is the fragment order (t_idx), zero padded
             const int nb = S.nb;
-            std::vector<double> Tp(S.T.size());
+            std::vector<double> Tp((size_t)S.nel * hsw::t_elem_doubles(nb), 0.0);
             for (size_t e = 0; e < (size_t)S.nel; ++e)
                 for (int n = 0; n < nb; ++n)
                     for (int m = 0; m < nb; ++m)
@@ -2233,7 +2233,9 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             h->d_qvol = dev_upload(S.qvol);
         } else {   // element tensors + source moments computed on the device (hsw_setup.cu)
             const size_t nb = (size_t)S.nb, nel = (size_t)S.nel;
-            CUDA_OK(cudaMalloc(&h->d_T, nel * nb * nb * 4 * sizeof(double)));
+            CUDA_OK(cudaMalloc(&h->d_T, nel * hsw::t_elem_doubles(S.nb) * sizeof(double)));
+            if (S.nb % 8 != 0)   // the tile padding is read by nobody, but keep it defined
+                CUDA_OK(cudaMemsetAsync(h->d_T, 0, nel * hsw::t_elem_doubles(S.nb) * sizeof(double), h->stream));
             CUDA_OK(cudaMalloc(&h->d_qvol, nel * nb * sizeof(double)));
             double* d_pts = dev_upload(S.mesh.pts);
             int* d_en = dev_upload(S.mesh.enodes);

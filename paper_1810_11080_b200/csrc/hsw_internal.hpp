@@ -37,20 +37,29 @@ constexpr int kMaxFacePoints = 64;    // (p+2)^2 for p <= 6
 #else
 #define HSW_HD
 #endif
-// Device layout of the element tensors T = (M, Gx, Gy, Gz), entry (row m, column n):
-// per (element, column) two planes of double2, (M, Gx) then (Gy, Gz), rows contiguous.
-// A warp loading rows 8 tr + g of columns 8 tc + 2 q + s (the DMMA fragment layout)
-// then reads whole 128-byte lines per plane (a [m][4] double4 layout fetched every
-// 32-byte sector twice through the two halves of its 256-bit load).
+// Device layout of the element tensors T = (M, Gx, Gy, Gz), entry (row m, column n): DMMA-fragment
+// order.  The n x n matrix is cut into 8x8 tiles (padded with zeros to a multiple of 8); per tile
+// (column-major over tiles), per column parity s = n & 1 and per plane ((M, Gx) | (Gy, Gz)) the 32
+// lanes' double2 values are contiguous: lane 4 (m & 7) + ((n & 7) >> 1).  A warp loading a tile in the
+// m8n8k4 accumulator layout (rows 8 tr + g, columns 8 tc + 2 q + s) therefore reads 512 contiguous
+// bytes per LDG.128 — one L1TEX wavefront per 128-byte line.  (The earlier planar layout
+// [column][plane][row] fetched the same sectors as four lines of eight lanes each: one wavefront per
+// 32-byte sector, measured 30.5 vs 76.2 B/clk/SM, tools/dmma_check/ldg_pattern.cu.)
+HSW_HD constexpr inline size_t t_tiles(int nb) { return (size_t)((nb + 7) / 8); }
+HSW_HD constexpr inline size_t t_elem_doubles(int nb) { return t_tiles(nb) * t_tiles(nb) * 256; }
+// double2 index, within one element, of plane p of entry (m, n)
+HSW_HD constexpr inline size_t t_idx2(int nb, int m, int n, int p) {
+    const size_t tile = (size_t)(n >> 3) * t_tiles(nb) + (size_t)(m >> 3);
+    return ((tile * 2 + (size_t)(n & 1)) * 2 + (size_t)p) * 32 + (size_t)(4 * (m & 7) + ((n & 7) >> 1));
+}
 HSW_HD inline size_t t_idx(size_t e, int nb, int m, int n, int k) {
-    return 2 * (((e * (size_t)nb + (size_t)n) * 2 + (size_t)(k >> 1)) * (size_t)nb + (size_t)m) + (size_t)(k & 1);
+    return e * t_elem_doubles(nb) + 2 * t_idx2(nb, m, n, k >> 1) + (size_t)(k & 1);
 }
 
 // Kernel-facing problem tables (device pointers), POD.
 struct DevProblem {
     int dim, p, nb, nfn, nqf, nfaces, nel, nd;
-    const double* T;          // planar, see t_idx: [E][n][2][m][2] (column n, plane (M, Gx) | (Gy, Gz),
-                              // row m) with G_k = -(d_k u)^T W u
+    const double* T;          // fragment order, see t_idx (planes (M, Gx) | (Gy, Gz)), G_k = -(d_k u)^T W u
     const double* sig_t;      // [E]
     const double* sig_s;      // [E]
     const double* bscale;     // [E] max_ij (sig_t |M| + |Gx| + |Gy| + |Gz|)_ij >= max |volume part of A(Omega)|:
