@@ -372,3 +372,49 @@ def test_pageable_host_sweep_equals_pinned_and_resident():
     # and one ordinate against the CPU oracle
     orc = O.OracleSolver(prob, cache_lu=False, check_rcond=False, active=[nd // 3])
     assert rel_l2(got_pageable[nd // 3], orc.sweep(nd // 3, phi, psi_old[nd // 3])) <= SWEEP_TOL
+
+
+# --------------------------------------------------------------------------- kernel variants
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import oracle as O
+import paper_1810_11080_b200 as pk
+from paper_1810_11080_b200 import problem as pb
+worst = 0.0
+for name, kw in {cases!r}:
+    prob = pb.config(name, **kw)
+    gpu = pk.SweepSolver(prob)
+    rng = np.random.default_rng(11)
+    phi = rng.uniform(0, 1, prob.num_dofs)
+    psi_old = rng.uniform(-0.5, 1, (prob.num_ordinates, prob.num_dofs))
+    got = gpu.sweep(-1, phi, psi_old)
+    ref = O.OracleSolver(prob).sweep_all(phi, psi_old)
+    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    assert gpu.total_lagged_edges() > 0 or name == "c3"
+    worst = max(worst, rel)
+    print(name, rel)
+assert worst <= 1e-10, worst
+print("VARIANT_OK", worst)
+"""
+
+_VARIANT_CASES = [("c3", dict(cells=6, n_mu=2, n_az=8)), ("c4", dict(cells=4, n_mu=2, n_az=8)),
+                  ("c5", dict(cells=3, n_mu=2, n_az=8)), ("c2", dict(cells=24, n_mu=2, n_az=8))]
+
+
+@pytest.mark.parametrize("env", [
+    {"HSW_LL": "1"},                      # left-looking static-pivot tile LU (3D shapes)
+    {"HSW_LL": "1", "HSW_SP_Q4": "1"},    # ... and the one-warp kernel at 3D Q4
+    {"HSW_SP_Q4": "1"},                   # right-looking static-pivot, one warp, 3D Q4
+    {"HSW_SP": "0"},                      # pivoted Gauss-Jordan kernels (the static-pivot fallback)
+    {"HSW_SP": "0", "HSW_D2": "0"},       # ... with the one-warp kernel at 3D Q4
+    {"HSW_TUNE": "2"},                    # pairs claimed at the top of the loop (no early prefetch)
+], ids=lambda e: "+".join(f"{k}={v}" for k, v in e.items()))
+def test_kernel_variants_match_oracle(env):
+    """The kernel selection is read from the environment once per process, so every opt-in /
+    fallback variant of the sweep kernel runs in its own process: one all-ordinate sweep of the
+    reduced 3D (and one 2D) configs against the CPU oracle, <= 1e-10."""
+    code = _VARIANT_SCRIPT.format(root=ROOT, cases=_VARIANT_CASES)
+    r = subprocess.run([os.sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "VARIANT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag, obj = sys.argv[1], sys.argv[2]
 o = os.path.join(ROOT, "gpurun_out", tag)
 P = os.path.join(ROOT, "profiles")
-KSUB = os.environ.get("KSUB", "Li3ELi3ELi2ELi5ELi12ELi8ELb0ELb1EE")   # the C4 production instantiation (static-pivot LU)
+KSUB = os.environ.get("KSUB", "Li3ELi3ELi2ELi5ELi12ELi8ELb0ELi1EE")   # the C4 production instantiation (static-pivot LU)
 PAIRS = 8388608
 
 
