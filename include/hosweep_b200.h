@@ -220,6 +220,10 @@ int hsw_synchronize(hsw_handle* h);
 void* hsw_stream(hsw_handle* h);
 /* Kernel launches issued by the last hsw_sweep_resident call. */
 int64_t hsw_last_launch_count(const hsw_handle* h);
+/* How many API calls were redone with the pivoted (partial-pivoting Gauss-Jordan) kernel because the
+ * static-pivot tile LU refused a local block (tiny pivot / large inverse tile); after the first one the
+ * handle keeps to the pivoted kernel.  0 on every BASELINE.json config. */
+int64_t hsw_pivot_fallbacks(const hsw_handle* h);
 /* Device time of the main sweep kernel launches of the last
  * hsw_sweep_resident call, measured with CUDA events on the handle's stream. */
 double hsw_last_sweep_kernel_ms(const hsw_handle* h);

@@ -26,7 +26,7 @@ EXPORTED = [
     "hsw_total_lagged_edges", "hsw_couplings", "hsw_interior_faces", "hsw_local_solve",
     "hsw_sweep", "hsw_sweep_device", "hsw_direct_oracle", "hsw_source_iteration", "hsw_balance",
     "hsw_balance_resident", "hsw_device_state", "hsw_sweep_resident", "hsw_synchronize", "hsw_stream",
-    "hsw_last_launch_count", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
+    "hsw_last_launch_count", "hsw_pivot_fallbacks", "hsw_last_sweep_kernel_ms", "hsw_debug_zero_block",
     "hsw_fp64_peak", "hsw_debug_flags", "hsw_set_state", "hsw_debug_profile",
     "hsw_shard_reset", "hsw_shard_sweep", "hsw_shard_sweep_host", "hsw_shard_phi_partial", "hsw_shard_psi_error",
     "hsw_shard_phi_norms", "hsw_shard_advance", "hsw_shard_psi", "hsw_debug_graph_order",
@@ -96,6 +96,8 @@ def load():
     L.hsw_stream.restype = vp
     L.hsw_last_launch_count.argtypes = [vp]
     L.hsw_last_launch_count.restype = i64
+    L.hsw_pivot_fallbacks.argtypes = [vp]
+    L.hsw_pivot_fallbacks.restype = i64
     L.hsw_last_sweep_kernel_ms.argtypes = [vp]
     L.hsw_last_sweep_kernel_ms.restype = C.c_double
     L.hsw_debug_zero_block.argtypes = [vp, C.c_int, C.c_int]

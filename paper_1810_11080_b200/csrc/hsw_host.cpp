@@ -3076,6 +3076,7 @@ int hsw_synchronize(hsw_handle* h) {
 
 void* hsw_stream(hsw_handle* h) { return h ? (void*)h->stream : nullptr; }
 int64_t hsw_last_launch_count(const hsw_handle* h) { return h ? h->last_launches : 0; }
+int64_t hsw_pivot_fallbacks(const hsw_handle* h) { return h ? h->pivot_fallbacks : 0; }
 double hsw_last_sweep_kernel_ms(const hsw_handle* h) { return h ? h->last_kernel_ms : 0.0; }
 
 int hsw_fp64_peak(int device, double* tflops) {

@@ -24,5 +24,5 @@ for name in (sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]):
     pairs = P.num_elements * P.num_ordinates
     n = P.block_size
     print(f"{name}: setup {setup:.1f}s levels {s.num_levels} sweep {m:.3f} ms  {pairs/m*1e3:.3e} solves/s  "
-          f"{flops(n)*pairs/m*1e-9:.2f} TFLOP/s(LU-alg)  launches {L.hsw_last_launch_count(s.handle)}", flush=True)
+          f"{flops(n)*pairs/m*1e-9:.2f} TFLOP/s(LU-alg)  launches {L.hsw_last_launch_count(s.handle)} pivot_fallbacks {L.hsw_pivot_fallbacks(s.handle)}", flush=True)
     s.close()
