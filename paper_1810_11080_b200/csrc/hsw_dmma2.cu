@@ -97,8 +97,20 @@ struct D2 {
     static constexpr int SM_ROWS = SM_PIVV + N;                       // [N] ints
     static constexpr int SM_PST = SM_ROWS + (N + 1) / 2;              // [NLP][PW] ints
     static constexpr int ELIM_END = SM_PST + (NLP * PW + 1) / 2;
-    static constexpr int X_END = FACE_END > ELIM_END ? FACE_END : ELIM_END;
-    static constexpr int SM_PAIR = (X_END + 2) & ~1;                  // + the claimed pair index slot
+    // static-pivot two-warp left-looking LU (SP): the negated inverse diagonal tiles, two tile
+    // transposition buffers per warp, the published -L~ tiles of the register tile-columns, the
+    // rhs / solution vector
+    static constexpr int XIS = 10;
+    static constexpr int SM_XI = SM_X;                                // [NTR][8][XIS]
+    static constexpr int SM_TB = SM_XI + NTR * 8 * XIS;               // [2 roles][2][8][XIS]
+    static constexpr int LRR = NTR - 1 - RB > 0 ? NTR - 1 - RB : 1;   // tile rows below the first register diagonal
+    static constexpr int LRC = NTC - 1 - RB > 0 ? NTC - 1 - RB : 1;   // register tile-columns with tiles below
+    static constexpr int SM_LR = SM_TB + 2 * 2 * 8 * XIS;             // [LRC][LRR][32][2]
+    static constexpr int SM_YX = SM_LR + LRC * LRR * 64;              // [NR]
+    static constexpr int LL_END = SM_YX + NR;
+    static constexpr int X_END0 = FACE_END > ELIM_END ? FACE_END : ELIM_END;
+    static constexpr int X_END = X_END0 > LL_END ? X_END0 : LL_END;
+    static constexpr int SM_PAIR = (X_END + 4) & ~1;                  // + the claimed pair index and the column counter
     static constexpr int TAB_INTS = NF * N + (N + 3) / 4 + NF * NFN + NSF + NS1;
     static constexpr int TAB_TRACE = ((TAB_INTS + 1) / 2 + 1) & ~1;
     static constexpr int TRS = NFN + (2 - NFN % 16 + 16) % 16;
@@ -174,7 +186,7 @@ __device__ __forceinline__ void tm_ld4x4w(uint32_t a0, uint32_t a1, uint32_t a2,
 __device__ __forceinline__ void pbar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void pbar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 
-template <int P, int NL_, int NT_, int PAIRS_>
+template <int P, int NL_, int NT_, int PAIRS_, bool SP_ = false>
 __global__ void __launch_bounds__(64 * PAIRS_, 1)
 dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const double* __restrict__ psi_old,
                    const double* psi_new_in, double* psi_out, int64_t psi_stride, const int* __restrict__ pairs,
@@ -257,6 +269,9 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     int* rowstep = reinterpret_cast<int*>(psm + G::SM_ROWS);
     int* s_pst = reinterpret_cast<int*>(psm + G::SM_PST);  // [NLP][PW]
     int* s_claim = reinterpret_cast<int*>(psm + G::SM_PAIR - 1);
+    // (SP) finished tile-columns of the pair: column k's owner publishes k + 1
+    volatile int* ndone = reinterpret_cast<volatile int*>(psm + G::SM_PAIR - 2);
+    if (SP_ && role == 0 && lane == 0) *ndone = 0;
     // own tile-columns: storage index of column c of this role
     // TMEM: tt = c - NL; own TMEM columns c = NL + t0 + 2 i, t0 = (NL ^ role) & 1 parity fix
     // role w owns the columns of parity w: SMEM columns w, w + 2, ...; TMEM columns NL + tt,
@@ -288,6 +303,8 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         const int e = pair / pr.nd, d = pair - (pair / pr.nd) * pr.nd;
         const double om0 = pr.omega[d * 4 + 0], om1 = pr.omega[d * 4 + 1], om2 = pr.omega[d * 4 + 2];
         const double amax = pr.bscale[e];
+        const int iex = SP_ ? ilogb(amax > 0.0 ? amax : 1.0) : 0;
+        const double isc = scalbn(1.0, -iex), iun = scalbn(1.0, iex);   // power of two ~ 1 / amax; isc * iun == 1
         if (role == 0 && !(pr.tune & 1)) {   // TMA L2 prefetch of the pair's element tensor
             constexpr unsigned TB = (unsigned)(t_elem_doubles(N) * sizeof(double));
             constexpr unsigned CH = 32768u;
@@ -602,6 +619,267 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
             __syncwarp();
         }
 
+        if constexpr (SP_) {
+        // ------------------------------------------------ static-pivot tile LU, left-looking, two warps
+        // A = L~ U over the 8x8 tiles (U unscaled, L~_ik = A_ik A_kk^-1; see the one-warp form in
+        // hsw_dmma1.cu).  A warp works through its OWN tile-columns in increasing order: column k is
+        // read once, receives c_i -= L~_ij U_jk for every finished column j < k in registers (the -L~
+        // tiles of the other warp's columns come from shared memory / TMEM, those of its register
+        // columns from the Lr buffer), its diagonal tile is inverted, the -L~ tiles below are formed
+        // and stored, and k + 1 is published in `ndone`.  Columns finish strictly in order, so the
+        // only wait is for the latest column of the other warp, and everything older is applied
+        // before that wait: a column's critical section is one update step, one tile inversion and
+        // the L~ tiles.  No row searches, no pivot-row gathers, 2/3 n^3 flops.
+        {
+            constexpr int XIS = G::XIS, NTC = G::NTC, LRR = G::LRR;
+            constexpr bool TAILC = N % 8 != 0;
+            static_assert(TAILC && NTC == NTR && NTR % 4 == 0, "two-warp static-pivot LU: rhs inside the last diagonal tile");
+            double* Xi = psm + G::SM_XI;
+            double* Tb = psm + G::SM_TB + role * (2 * 8 * XIS);
+            double* Lr = psm + G::SM_LR;
+            double* yx = psm + G::SM_YX;
+            unsigned xmaxh = 0u;
+            int tbsel = 0;
+            auto tb_put = [&](double p0, double p1) {
+                *reinterpret_cast<double2*>(Tb + tbsel + g * XIS + 2 * q) = make_double2(p0, p1);
+            };
+            auto tb_get = [&](double& b0, double& b1) {
+                __syncwarp();
+                b0 = Tb[tbsel + (2 * q) * XIS + g];
+                b1 = Tb[tbsel + (2 * q + 1) * XIS + g];
+                tbsel ^= 8 * XIS;
+            };
+            auto st4 = [&](uint32_t a, double v0, double v1) {
+                asm volatile("{\n .reg .b32 t<4>;\n mov.b64 {t0,t1}, %1;\n mov.b64 {t2,t3}, %2;\n"
+                             " tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {t0,t1,t2,t3};\n}" ::"r"(a), "d"(v0), "d"(v1) : "memory");
+            };
+            // tile (tr, k) of an own column k < RB
+            auto home_store = [&](int tr, int k, double v0, double v1) {
+                if (k < NL) *reinterpret_cast<double2*>(AL + ((k * NTR + tr) * 32 + lsw) * 2) = make_double2(v0, v1);
+                else st4(tmw + (uint32_t)(((k - NL) * NTR + tr) * 4), v0, v1);
+            };
+            auto lr_tile = [&](int c, int tr) { return Lr + (((c - RB) * LRR + (tr - RB - 1)) * 32 + lane) * 2; };
+            double c[NTR][2];
+#pragma unroll 1
+            for (int k = role; k < NTC; k += 2) {
+                // (1) the column
+                if (k < NL) {
+#pragma unroll
+                    for (int tr = 0; tr < NTR; ++tr) {
+                        const double2 v = *reinterpret_cast<const double2*>(AL + ((k * NTR + tr) * 32 + lsw) * 2);
+                        c[tr][0] = v.x;
+                        c[tr][1] = v.y;
+                    }
+                } else if (k < RB) {
+#pragma unroll
+                    for (int grp = 0; grp < NTR / 4; ++grp) {
+                        double v[4][2];
+                        tm_get4(k - NL, grp, v);
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {
+                            c[4 * grp + k4][0] = v[k4][0];
+                            c[4 * grp + k4][1] = v[k4][1];
+                        }
+                    }
+                } else {
+                    static_row<0, NRW>((k - RB - r0) >> 1, [&](auto J_) {
+                        constexpr int jr = decltype(J_)::value;
+#pragma unroll
+                        for (int tr = 0; tr < NTR; ++tr) {
+                            c[tr][0] = acc[jr][tr][0];
+                            c[tr][1] = acc[jr][tr][1];
+                        }
+                    });
+                }
+                // (2) left-looking updates with the finished columns j < k
+                if (k > 0) {
+                    double b0, b1;
+                    tb_put(c[0][0], c[0][1]);   // row 0 never changes: U_0k as assembled
+                    tb_get(b0, b1);
+#pragma unroll 1
+                    for (int j = 0; j < k; ++j) {
+                        if ((j ^ role) & 1) {   // the other warp's column: published?
+                            if (*ndone <= j) {
+                                const long long t_wait = clock64();
+                                while (*ndone <= j) {
+                                    // ~4 s without the other warp's column: flag it instead of hanging
+                                    if (clock64() - t_wait > (1ll << 33)) {
+                                        if (done_flags) atomicExch(done_flags + (size_t)pr.nel * pr.nd, 1u);
+                                        break;
+                                    }
+                                }
+                            }
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                            __threadfence_block();
+                            __syncwarp();
+                        }
+                        const bool more = j + 1 < k;
+                        static_row<0, NTC - 1>(j, [&](auto J_) {
+                            constexpr int J = decltype(J_)::value;
+                            constexpr int G0 = (J + 1) / 4;
+                            double nb0 = 0.0, nb1 = 0.0;
+#pragma unroll
+                            for (int grp = G0; grp < NTR / 4; ++grp) {
+                                double lf[4][2];
+                                if constexpr (J < NL) {
+#pragma unroll
+                                    for (int k4 = 0; k4 < 4; ++k4)
+                                        if (4 * grp + k4 > J) {
+                                            const double2 l = *reinterpret_cast<const double2*>(
+                                                AL + ((J * NTR + 4 * grp + k4) * 32 + lsw) * 2);
+                                            lf[k4][0] = l.x;
+                                            lf[k4][1] = l.y;
+                                        }
+                                } else if constexpr (J < RB) {
+                                    tm_get4(J - NL, grp, lf);
+                                } else {
+#pragma unroll
+                                    for (int k4 = 0; k4 < 4; ++k4)
+                                        if (4 * grp + k4 > J) {
+                                            const double2 l = *reinterpret_cast<const double2*>(lr_tile(J, 4 * grp + k4));
+                                            lf[k4][0] = l.x;
+                                            lf[k4][1] = l.y;
+                                        }
+                                }
+#pragma unroll
+                                for (int k4 = 0; k4 < 4; ++k4)
+                                    if (4 * grp + k4 > J) {
+                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lf[k4][0], b0);
+                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lf[k4][1], b1);
+                                    }
+                                if (grp == G0 && more) {   // U_{j+1,k} is final: store it, transpose it for the next step
+                                    if (k < RB) home_store(J + 1, k, c[J + 1][0], c[J + 1][1]);
+                                    tb_put(c[J + 1][0], c[J + 1][1]);
+                                    tb_get(nb0, nb1);
+                                }
+                            }
+                            b0 = nb0;
+                            b1 = nb1;
+                        });
+                    }
+                }
+                // (3) the diagonal tile's inverse
+                {
+                    double d0 = 0.0, d1 = 0.0;
+                    static_row<0, NTR>(k, [&](auto T_) {
+                        constexpr int t = decltype(T_)::value;
+                        d0 = c[t][0];
+                        d1 = c[t][1];
+                    });
+                    if (k == NTR - 1) {   // padding rows, the rhs and padding columns -> identity
+                        const int r = 8 * k + g, cc = 8 * k + 2 * q;
+                        if (cc >= N) d0 = r == cc ? iun : 0.0;
+                        if (cc + 1 >= N) d1 = r == cc + 1 ? iun : 0.0;
+                    }
+                    inv8_tile(d0, d1, isc, g, q);
+                    const unsigned h0 = (unsigned)__double2hiint(d0) & 0x7fffffffu, h1 = (unsigned)__double2hiint(d1) & 0x7fffffffu;
+                    xmaxh = max(xmaxh, max(h0, h1));
+                    *reinterpret_cast<double2*>(Xi + k * 8 * XIS + g * XIS + 2 * q) = make_double2(-d0, -d1);
+                    __syncwarp();
+                }
+                // (4) -L~_ik = A_ik (-X), i > k, stored over the column's tiles (register columns: Lr)
+                if (k < NTR - 1) {
+                    static_row<0, NTR - 1>(k, [&](auto K_) {
+                        constexpr int K = decltype(K_)::value;
+                        const double xb0 = Xi[K * 8 * XIS + (2 * q) * XIS + g], xb1 = Xi[K * 8 * XIS + (2 * q + 1) * XIS + g];
+#pragma unroll
+                        for (int tr = K + 1; tr < NTR; ++tr) {
+                            double l0 = 0.0, l1 = 0.0;
+                            mma884(l0, l1, c[tr][0], xb0);
+                            mma884(l0, l1, c[tr][1], xb1);
+                            if constexpr (K < RB) home_store(tr, K, l0, l1);
+                            else *reinterpret_cast<double2*>(lr_tile(K, tr)) = make_double2(l0, l1);
+                        }
+                    });
+                }
+                // a register column keeps its U tiles (rows <= k) in acc
+                if (k >= RB) {
+                    static_row<0, NRW>((k - RB - r0) >> 1, [&](auto J_) {
+                        constexpr int jr = decltype(J_)::value;
+#pragma unroll
+                        for (int tr = 0; tr < NTR; ++tr) {
+                            acc[jr][tr][0] = c[tr][0];
+                            acc[jr][tr][1] = c[tr][1];
+                        }
+                    });
+                }
+                // (5) publish the column
+                tm_wait_st();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) *ndone = k + 1;
+            }
+            {
+                const unsigned xm = __reduce_max_sync(FULL, xmaxh);
+                if (!(__hiloint2double((int)xm, 0) * amax <= 1e5) && lane == 0)
+                    atomicMin(err_key + 1, (unsigned long long)pair);
+            }
+            // ---------------------------------------------- back substitution, column by column:
+            // x_k = X_k y_k, then y_i -= U_ik x_k (i < k) by the column's owner; y and x share yx
+            if (rhs_owner && q == QR) {
+#pragma unroll
+                for (int tr = 0; tr < NTR; ++tr) yx[8 * tr + g] = 8 * tr + g < N ? acc[G::JR][tr][SR] : 0.0;
+            }
+            pbar_sync(bid + 1);
+#pragma unroll 1
+            for (int k = NTR - 1; k >= 0; --k) {
+                if ((k & 1) == role) {
+                    const double2 z = *reinterpret_cast<const double2*>(yx + 8 * k + 2 * q);
+                    const double2 xn = *reinterpret_cast<const double2*>(Xi + k * 8 * XIS + g * XIS + 2 * q);
+                    double t = fma(xn.x, z.x, xn.y * z.y);
+                    t += __shfl_xor_sync(FULL, t, 1);
+                    t += __shfl_xor_sync(FULL, t, 2);
+                    __syncwarp();
+                    if (q == 0) yx[8 * k + g] = 8 * k + g < N ? -t : 0.0;
+                    __syncwarp();
+                    const double2 x2 = *reinterpret_cast<const double2*>(yx + 8 * k + 2 * q);
+                    auto axpy = [&](int i, double u0, double u1) {
+                        double part = fma(u0, x2.x, u1 * x2.y);
+                        part += __shfl_xor_sync(FULL, part, 1);
+                        part += __shfl_xor_sync(FULL, part, 2);
+                        if (q == 0) yx[8 * i + g] -= part;
+                    };
+                    if (k < NL) {
+#pragma unroll 1
+                        for (int i = 0; i < k; ++i) {
+                            const double2 u = *reinterpret_cast<const double2*>(AL + ((k * NTR + i) * 32 + lsw) * 2);
+                            axpy(i, u.x, u.y);
+                        }
+                    } else if (k < RB) {
+#pragma unroll 1
+                        for (int grp = 0; 4 * grp < k; ++grp) {
+                            double v[4][2];
+                            tm_get4(k - NL, grp, v);
+#pragma unroll
+                            for (int k4 = 0; k4 < 4; ++k4)
+                                if (4 * grp + k4 < k) axpy(4 * grp + k4, v[k4][0], v[k4][1]);
+                        }
+                    } else {
+                        static_row<0, NRW>((k - RB - r0) >> 1, [&](auto J_) {
+                            constexpr int jr = decltype(J_)::value;
+#pragma unroll
+                            for (int i = 0; i < NTR - 1; ++i)
+                                if (i < k) axpy(i, acc[jr][i][0], acc[jr][i][1]);
+                        });
+                    }
+                    __syncwarp();
+                }
+                pbar_sync(bid + 1 + (k & 1));
+            }
+            if (role == 0 && lane == 0) *ndone = 0;   // both warps are past their last read of it
+            if (rhs_owner) {
+                double* out = rhs_given ? psi_out : psi_out + (size_t)d * psi_stride + (size_t)e * N;
+                for (int r = lane; r < N; r += 32) out[r] = yx[r];
+                if (done_flags) {
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(done_flags + pair), "r"(epoch) : "memory");
+                }
+            }
+        }
+        } else {
         // ------------------------------------------------ blocked Gauss-Jordan, two warps
         unsigned am[RP];
         bool singular = false;
@@ -921,6 +1199,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(done_flags + pair), "r"(epoch) : "memory");
             }
         }
+        }
         __syncwarp();
     }
     if (NT > 0) {
@@ -930,7 +1209,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     }
 }
 
-template <int P, int NL, int NT, int PAIRS>
+template <int P, int NL, int NT, int PAIRS, bool SP = false>
 void launch_dmma2(const DevProblem& pr, const double* src, const double* psi_old, const double* psi_new_in,
                   double* psi_out, int64_t stride, const int* pairs, int npairs, const double* rhs_given,
                   unsigned long long* err, int64_t zero_pair, cudaStream_t st, unsigned* done_flags, unsigned epoch) {
@@ -940,18 +1219,18 @@ void launch_dmma2(const DevProblem& pr, const double* src, const double* psi_old
     int dev = 0;
     D2CHECK(cudaGetDevice(&dev));
     const int max_blocks = per_device_once(slots, mu, dev, [&] {
-        D2CHECK(cudaFuncSetAttribute(dmma2_sweep_kernel<P, NL, NT, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        D2CHECK(cudaFuncSetAttribute(dmma2_sweep_kernel<P, NL, NT, PAIRS, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)G::SMEM));
         int sms = 0, per_sm = 0;
         D2CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        D2CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma2_sweep_kernel<P, NL, NT, PAIRS>, G::THREADS,
+        D2CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dmma2_sweep_kernel<P, NL, NT, PAIRS, SP>, G::THREADS,
                                                               G::SMEM));
         if (per_sm < 1) throw Error(-8, "dmma2 kernel does not fit on an SM");
         return sms * (per_sm > 1 ? 1 : per_sm);   // one CTA per SM: it owns all TMEM columns
     });
     int blocks = (npairs + G::PAIRS - 1) / G::PAIRS;
     if (blocks > max_blocks) blocks = max_blocks;
-    dmma2_sweep_kernel<P, NL, NT, PAIRS><<<blocks, G::THREADS, G::SMEM, st>>>(
+    dmma2_sweep_kernel<P, NL, NT, PAIRS, SP><<<blocks, G::THREADS, G::SMEM, st>>>(
         pr, src, psi_old, psi_new_in, psi_out, stride, pairs, npairs, rhs_given, err, zero_pair, done_flags, epoch);
     D2CHECK(cudaGetLastError());
 }
@@ -964,12 +1243,14 @@ bool dev_dmma2_supported(int dim, int p) { return dim == 3 && p == 4; }
 
 void dev_dmma2_sweep(const DevProblem& P, const double* src, const double* psi_old, double* psi_new, int64_t stride,
                      const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream,
-                     unsigned* done_flags, unsigned epoch) {
+                     unsigned* done_flags, unsigned epoch, bool static_pivot) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (P.dim == 3 && P.p == 4)
+    if (P.dim == 3 && P.p == 4 && static_pivot)
+        launch_dmma2<4, 4, 8, 4, true>(P, src, psi_old, psi_new, psi_new, stride, pairs, npairs, nullptr, err_key,
+                                       zero_pair, st, done_flags, epoch);
+    else if (P.dim == 3 && P.p == 4)
         launch_dmma2<4, 4, 8, 4>(P, src, psi_old, psi_new, psi_new, stride, pairs, npairs, nullptr, err_key, zero_pair,
                                  st, done_flags, epoch);
-
     else
         throw Error(-1, "dmma2 kernel: unsupported (dim, order)");
 }

@@ -1804,33 +1804,42 @@ int kernel_choice_for(int dim, int p) {
     return (!force_dmma && dev_dmma1_supported(dim, p)) ? 3 : 2;
 }
 
-// Static-pivot tile LU (hsw_dmma1.cu, SP instantiations): the production sweep kernel
-// unless a block of this problem was refused (need_pivot) or HSW_SP=0.
-// HSW_SP_Q4=0/1 selects it for the 3D Q4 shape (else the two-warp pivoted kernel).
+// Static-pivot tile LU: the production sweep kernels unless a block of this problem was refused
+// (need_pivot) or HSW_SP=0.  hsw_dmma1.cu (one warp per pair) for every shape but 3D Q4, where the
+// two-warp kernel's left-looking static-pivot form runs (hsw_dmma2.cu); HSW_SP_Q4=1 selects the
+// one-warp kernel there, HSW_SP_Q4=0 the pivoted two-warp kernel.
+int sp_q4_env() {
+    static const int q4 = [] {
+        const char* e = std::getenv("HSW_SP_Q4");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return q4;
+}
 bool static_pivot(const hsw_handle* h) {
     static const int env = [] {
         const char* e = std::getenv("HSW_SP");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    static const int q4 = [] {
-        const char* e = std::getenv("HSW_SP_Q4");
-        return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
     if (env == 0 || h->need_pivot) return false;
     const int kc = kernel_choice_for(h->S.dim, h->S.p);
-    if (kc == 4) return q4 == 1;
+    if (kc == 4) return sp_q4_env() != 0;
     return kc == 3;
 }
-// 5: dmma1 static-pivot, 4: dmma2, 3: dmma1 pivoted, 2: dmma
-int kernel_choice(const hsw_handle* h) { return static_pivot(h) ? 5 : kernel_choice_for(h->S.dim, h->S.p); }
+// 6: dmma2 static-pivot, 5: dmma1 static-pivot, 4: dmma2, 3: dmma1 pivoted, 2: dmma
+int kernel_choice(const hsw_handle* h) {
+    const int kc = kernel_choice_for(h->S.dim, h->S.p);
+    if (!static_pivot(h)) return kc;
+    return kc == 4 && sp_q4_env() != 1 ? 6 : 5;
+}
 
 void sweep_launch(hsw_handle* h, const double* psi_old, double* psi_new, const int* pairs, int n) {
     const int kc = kernel_choice(h);
     if (kc == 5)
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
                         nullptr, 0, true);
-    else if (kc == 4)
-        dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
+    else if (kc == 4 || kc == 6)
+        dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
+                        nullptr, 0, kc == 6);
     else if (kc == 3)
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream);
     else
@@ -1888,9 +1897,9 @@ void dataflow_sweep(hsw_handle* h, const double* psi_old, double* psi_new, const
     const unsigned ep = next_epoch(h);
     CUDA_OK(cudaMemsetAsync(h->d_done + (size_t)h->S.nel * h->S.nd + 1, 0, sizeof(unsigned), h->stream));
     const int kc = kernel_choice(h);
-    if (kc == 4)
+    if (kc == 4 || kc == 6)
         dev_dmma2_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
-                        h->d_done, ep);
+                        h->d_done, ep, kc == 6);
     else
         dev_dmma1_sweep(h->P, h->d_src, psi_old, psi_new, (int64_t)h->N, pairs, n, h->d_err, h->zero_pair, h->stream,
                         h->d_done, ep, kc == 5);
