@@ -43,7 +43,7 @@ namespace {
             throw Error(-8, std::string("CUDA: ") + cudaGetErrorString(_e) + " at " #x);       \
     } while (0)
 
-template <int P, int NL_, int NT_, int PAIRS_>
+template <int P, int NL_, int NT_, int PAIRS_, bool SP_ = false>
 struct D2 {
     static constexpr int PW = 4;                        // panel width (one m8n8k4 k-chunk)
     static constexpr int N1 = P + 1;
@@ -62,7 +62,8 @@ struct D2 {
     static_assert(TCR >= RB, "the rhs tile-column must be register resident");
     static constexpr int PAIRS = PAIRS_;
     static_assert(PAIRS % 4 == 0, "a pair's two warps must share a TMEM lane quarter");
-    static_assert(1 + 3 * PAIRS <= 16, "three named barriers per pair (ids 1..15)");
+    static constexpr int NBAR = SP_ ? 1 : 3;            // named barriers per pair (the static-pivot form needs one)
+    static_assert(1 + NBAR * PAIRS <= 16, "named barriers per pair (ids 1..15)");
     static constexpr int WARPS = 2 * PAIRS;
     static constexpr int THREADS = 32 * WARPS;
     static constexpr int PPQ = PAIRS / 4;               // pairs per TMEM lane quarter
@@ -108,8 +109,8 @@ struct D2 {
     static constexpr int SM_LR = SM_TB + 2 * 2 * 8 * XIS;             // [LRC][LRR][32][2]
     static constexpr int SM_YX = SM_LR + LRC * LRR * 64;              // [NR]
     static constexpr int LL_END = SM_YX + NR;
-    static constexpr int X_END0 = FACE_END > ELIM_END ? FACE_END : ELIM_END;
-    static constexpr int X_END = X_END0 > LL_END ? X_END0 : LL_END;
+    static constexpr int EL_END = SP_ ? LL_END : ELIM_END;
+    static constexpr int X_END = FACE_END > EL_END ? FACE_END : EL_END;
     static constexpr int SM_PAIR = (X_END + 4) & ~1;                  // + the claimed pair index and the column counter
     static constexpr int TAB_INTS = NF * N + (N + 3) / 4 + NF * NFN + NSF + NS1;
     static constexpr int TAB_TRACE = ((TAB_INTS + 1) / 2 + 1) & ~1;
@@ -192,7 +193,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                    const double* psi_new_in, double* psi_out, int64_t psi_stride, const int* __restrict__ pairs,
                    int npairs, const double* __restrict__ rhs_given, unsigned long long* err_key, int64_t zero_pair,
                    unsigned* done_flags, unsigned epoch) {
-    using G = D2<P, NL_, NT_, PAIRS_>;
+    using G = D2<P, NL_, NT_, PAIRS_, SP_>;
     constexpr int PW = G::PW, N = G::N, NTR = G::NTR, NL = G::NL, NT = G::NT, RB = G::RB, NRW = G::NRW;
     constexpr int NR = G::NR, RP = G::RP, NPANEL = G::NPANEL, TCR = G::TCR, QR = G::QR, SR = G::SR;
     constexpr int NFN = G::NFN, NF = G::NF, NQ1 = G::NQ1, NQF = G::NQF, N1 = G::N1, NSF = G::NSF, NS1 = G::NS1;
@@ -208,7 +209,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
     const bool rhs_owner = role == G::RHS_ROLE;
     // named barrier ids of this pair: 1 + 3 ps + {0: pair start, each outflow face block, faces
     // done (both sync); 1, 2: panel parity 0 / 1 (the producer arrives, the other syncs)}
-    const int bid = 1 + 3 * ps;
+    const int bid = 1 + G::NBAR * ps;
     if (NT > 0) {
         if (warp == 0) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -614,7 +615,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         __syncwarp();
         // faces done by both warps: the face scratch becomes the elimination buffers
         pbar_sync(bid);
-        if (owner_of(0) == role) {   // the first factoring warp; the other reads steps only after a panel barrier
+        if (!SP_ && owner_of(0) == role) {   // the first factoring warp; the other reads steps only after a panel barrier
             for (int r = lane; r < N; r += 32) rowstep[r] = -1;
             __syncwarp();
         }
@@ -633,7 +634,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
         {
             constexpr int XIS = G::XIS, NTC = G::NTC, LRR = G::LRR;
             constexpr bool TAILC = N % 8 != 0;
-            static_assert(TAILC && NTC == NTR && NTR % 4 == 0, "two-warp static-pivot LU: rhs inside the last diagonal tile");
+            static_assert(NTR % 4 == 0, "two-warp static-pivot LU: whole 4-tile groups");
             double* Xi = psm + G::SM_XI;
             double* Tb = psm + G::SM_TB + role * (2 * 8 * XIS);
             double* Lr = psm + G::SM_LR;
@@ -758,15 +759,15 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         });
                     }
                 }
-                // (3) the diagonal tile's inverse
-                {
+                // (3) the diagonal tile's inverse (the rhs-only tile-column of n % 8 == 0 has none)
+                if (k < NTR) {
                     double d0 = 0.0, d1 = 0.0;
                     static_row<0, NTR>(k, [&](auto T_) {
                         constexpr int t = decltype(T_)::value;
                         d0 = c[t][0];
                         d1 = c[t][1];
                     });
-                    if (k == NTR - 1) {   // padding rows, the rhs and padding columns -> identity
+                    if (TAILC && k == NTR - 1) {   // padding rows, the rhs and padding columns -> identity
                         const int r = 8 * k + g, cc = 8 * k + 2 * q;
                         if (cc >= N) d0 = r == cc ? iun : 0.0;
                         if (cc + 1 >= N) d1 = r == cc + 1 ? iun : 0.0;
@@ -816,12 +817,15 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     atomicMin(err_key + 1, (unsigned long long)pair);
             }
             // ---------------------------------------------- back substitution, column by column:
-            // x_k = X_k y_k, then y_i -= U_ik x_k (i < k) by the column's owner; y and x share yx
+            // x_k = X_k y_k, then y_i -= U_ik x_k (i < k) by the column's owner; y and x share yx.
+            // (Measured slower at C5: splitting the rows of the shared-memory / TMEM columns between
+            // both warps, two barriers per column, 804 vs 778 ms; claiming the next pair here to
+            // prefetch its 512 KB tensor early, 833 ms: 592 pairs' tensors do not fit the L2.)
             if (rhs_owner && q == QR) {
 #pragma unroll
                 for (int tr = 0; tr < NTR; ++tr) yx[8 * tr + g] = 8 * tr + g < N ? acc[G::JR][tr][SR] : 0.0;
             }
-            pbar_sync(bid + 1);
+            pbar_sync(bid);
 #pragma unroll 1
             for (int k = NTR - 1; k >= 0; --k) {
                 if ((k & 1) == role) {
@@ -865,7 +869,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                     }
                     __syncwarp();
                 }
-                pbar_sync(bid + 1 + (k & 1));
+                pbar_sync(bid);
             }
             if (role == 0 && lane == 0) *ndone = 0;   // both warps are past their last read of it
             if (rhs_owner) {
@@ -1213,7 +1217,7 @@ template <int P, int NL, int NT, int PAIRS, bool SP = false>
 void launch_dmma2(const DevProblem& pr, const double* src, const double* psi_old, const double* psi_new_in,
                   double* psi_out, int64_t stride, const int* pairs, int npairs, const double* rhs_given,
                   unsigned long long* err, int64_t zero_pair, cudaStream_t st, unsigned* done_flags, unsigned epoch) {
-    using G = D2<P, NL, NT, PAIRS>;
+    using G = D2<P, NL, NT, PAIRS, SP>;
     static int slots[64] = {};
     static std::mutex mu;
     int dev = 0;
@@ -1245,7 +1249,10 @@ void dev_dmma2_sweep(const DevProblem& P, const double* src, const double* psi_o
                      const int* pairs, int npairs, unsigned long long* err_key, int64_t zero_pair, void* stream,
                      unsigned* done_flags, unsigned epoch, bool static_pivot) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (P.dim == 3 && P.p == 4 && static_pivot)
+    if (P.dim == 3 && P.p == 3 && static_pivot)   // C4 shape: eight two-warp pairs per SM (HSW_D2_Q3=1)
+        launch_dmma2<3, 1, 6, 8, true>(P, src, psi_old, psi_new, psi_new, stride, pairs, npairs, nullptr, err_key,
+                                       zero_pair, st, done_flags, epoch);
+    else if (P.dim == 3 && P.p == 4 && static_pivot)
         launch_dmma2<4, 4, 8, 4, true>(P, src, psi_old, psi_new, psi_new, stride, pairs, npairs, nullptr, err_key,
                                        zero_pair, st, done_flags, epoch);
     else if (P.dim == 3 && P.p == 4)

@@ -1829,6 +1829,9 @@ bool static_pivot(const hsw_handle* h) {
 int kernel_choice(const hsw_handle* h) {
     const int kc = kernel_choice_for(h->S.dim, h->S.p);
     if (!static_pivot(h)) return kc;
+    // HSW_D2_Q3=1: the two-warp static-pivot kernel at 3D Q3 too (eight pairs per SM)
+    static const bool d2q3 = [] { const char* e = std::getenv("HSW_D2_Q3"); return e && e[0] == '1'; }();
+    if (d2q3 && h->S.dim == 3 && h->S.p == 3) return 6;
     return kc == 4 && sp_q4_env() != 1 ? 6 : 5;
 }
 

@@ -406,6 +406,8 @@ _VARIANT_CASES = [("c3", dict(cells=6, n_mu=2, n_az=8)), ("c4", dict(cells=4, n_
     {"HSW_LL": "1"},                      # left-looking static-pivot tile LU (3D shapes)
     {"HSW_LL": "1", "HSW_SP_Q4": "1"},    # ... and the one-warp kernel at 3D Q4
     {"HSW_SP_Q4": "1"},                   # right-looking static-pivot, one warp, 3D Q4
+    {"HSW_SP_Q4": "0"},                   # pivoted two-warp Gauss-Jordan at 3D Q4 (static pivot elsewhere)
+    {"HSW_D2_Q3": "1"},                   # two-warp left-looking static-pivot kernel at 3D Q3 too
     {"HSW_SP": "0"},                      # pivoted Gauss-Jordan kernels (the static-pivot fallback)
     {"HSW_SP": "0", "HSW_D2": "0"},       # ... with the one-warp kernel at 3D Q4
     {"HSW_TUNE": "2"},                    # pairs claimed at the top of the loop (no early prefetch)
