@@ -141,7 +141,7 @@ M = [f"# {tag}: sweep kernel profiles (C4: hsw_dmma1, one warp per pair; C5: hsw
      f"{tr['l1tex__t_sector_hit_rate.pct']:.1f} %, L2 hit {tr['lts__t_sector_hit_rate.pct']:.1f} %.", ""]
 M += ncu_section("c4", "c4", "hsw_dmma1.cu", obj, KSUB, "C4 (hsw_dmma1)")
 M += [""]
-M += ncu_section("c5", "c5", "hsw_dmma2.cu", obj.replace("hsw_dmma1", "hsw_dmma2"), "dmma2_sweep_kernelILi4ELi4ELi8ELi4E",
+M += ncu_section("c5", "c5", "hsw_dmma2.cu", obj.replace("hsw_dmma1", "hsw_dmma2"), "dmma2_sweep_kernelILi4ELi4ELi8ELi4ELb1E",
                  "C5 (hsw_dmma2)")
 open(f"{P}/{tag}_ncu.md", "w").write("\n".join(M) + "\n")
 print("wrote", tag, "profiles")
