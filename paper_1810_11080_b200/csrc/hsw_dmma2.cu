@@ -375,19 +375,17 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         combine(gi_tt(gi), gi % GPC, b);
                     }
                 } else {
-                    // loads two groups ahead (24 KB in flight per warp; the accumulator registers are
-                    // not live yet), three groups per (rolled) iteration
-                    double4 b0[4][2], b1[4][2], b2[4][2];
+                    // loads one group ahead, two groups per (rolled) iteration: a small code
+                    // footprint (eight warps per SM share the instruction cache).  Two groups ahead
+                    // (three 64-register buffers) spills in this loop: C5 1501 vs 766 ms.
+                    double4 b0[4][2], b1[4][2];
                     ldgrp(gi_tt(0), 0, b0);
-                    if (1 < NGR) ldgrp(gi_tt(1), 1 % GPC, b1);
 #pragma unroll 1
-                    for (int gi = 0; gi < NGR; gi += 3) {
-                        if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, b2);
+                    for (int gi = 0; gi < NGR; gi += 2) {
+                        if (gi + 1 < NGR) ldgrp(gi_tt(gi + 1), (gi + 1) % GPC, b1);
                         combine(gi_tt(gi), gi % GPC, b0);
-                        if (gi + 3 < NGR) ldgrp(gi_tt(gi + 3), (gi + 3) % GPC, b0);
+                        if (gi + 2 < NGR) ldgrp(gi_tt(gi + 2), (gi + 2) % GPC, b0);
                         if (gi + 1 < NGR) combine(gi_tt(gi + 1), (gi + 1) % GPC, b1);
-                        if (gi + 4 < NGR) ldgrp(gi_tt(gi + 4), (gi + 4) % GPC, b1);
-                        if (gi + 2 < NGR) combine(gi_tt(gi + 2), (gi + 2) % GPC, b2);
                     }
                 }
             }
