@@ -5,10 +5,12 @@ import collections, os, re, subprocess, sys
 out = sys.argv[1]
 objd = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                            "paper_1810_11080_b200", "lib", "obj")
-KERNELS = [("hsw_dmma1.cu.o", "Li3ELi3ELi2ELi5ELi12ELi4ELb0EE", "C4: dmma1_sweep_kernel<3,3,2,5,12,4>"),
-           ("hsw_dmma1.cu.o", "Li3ELi2ELi2ELi0ELi20ELi4ELb0EE", "C3: dmma1_sweep_kernel<3,2,2,0,20,4>"),
-           ("hsw_dmma1.cu.o", "Li2ELi3ELi3ELi0ELi16ELi4ELb0EE", "C2: dmma1_sweep_kernel<2,3,3,0,16,4>"),
-           ("hsw_dmma2.cu.o", "dmma2_sweep_kernelILi4ELi4ELi8ELi4E", "C5: dmma2_sweep_kernel<4,4,8,4>")]
+KERNELS = [("hsw_dmma1.cu.o", "Li3ELi3ELi2ELi5ELi12ELi8ELb0ELi1EE", "C4: dmma1_sweep_kernel<3,3,2,5,12,8,SP=1> (static-pivot LU)"),
+           ("hsw_dmma1.cu.o", "Li3ELi2ELi2ELi0ELi20ELi8ELb0ELi1EE", "C3: dmma1_sweep_kernel<3,2,2,0,20,8,SP=1>"),
+           ("hsw_dmma1.cu.o", "Li2ELi3ELi3ELi0ELi16ELi8ELb0ELi1EE", "C2: dmma1_sweep_kernel<2,3,3,0,16,8,SP=1>"),
+           ("hsw_dmma2.cu.o", "dmma2_sweep_kernelILi4ELi4ELi8ELi4ELb1E", "C5: dmma2_sweep_kernel<4,4,8,4,SP> (two-warp left-looking LU)"),
+           ("hsw_dmma1.cu.o", "Li3ELi3ELi2ELi5ELi12ELi4ELb0ELi0EE", "fallback C4: dmma1_sweep_kernel<3,3,2,5,12,4,SP=0> (pivoted Gauss-Jordan)"),
+           ("hsw_dmma2.cu.o", "dmma2_sweep_kernelILi4ELi4ELi8ELi4ELb0E", "fallback C5: dmma2_sweep_kernel<4,4,8,4> (pivoted Gauss-Jordan)")]
 FOCUS = ["DMMA", "LDTM", "STTM", "UTCBAR", "UBLKPF", "UBLKCP", "UTMALDG", "DFMA", "DMUL", "DADD", "LDS", "STS",
          "LDG", "STG", "SHFL", "CREDUX", "BAR", "MEMBAR", "STL", "LDL"]
 L = ["# SASS opcode counts of the production sweep kernels (static, `cuobjdump -sass`)", "",
