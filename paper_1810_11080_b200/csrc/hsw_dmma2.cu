@@ -718,36 +718,58 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                         const bool more = j + 1 < k;
                         static_row<0, NTC - 1>(j, [&](auto J_) {
                             constexpr int J = decltype(J_)::value;
-                            constexpr int G0 = (J + 1) / 4;
+                            constexpr int G0 = (J + 1) / 4, NG = NTR / 4;
                             double nb0 = 0.0, nb1 = 0.0;
-#pragma unroll
-                            for (int grp = G0; grp < NTR / 4; ++grp) {
-                                double lf[4][2];
+                            // the -L~ tiles of group grp + 1 are requested before the DMMAs of group grp
+                            // (TMEM: asynchronous tcgen05.ld, waited for just before its use)
+                            uint32_t rt[2][16];
+                            double lfs[2][4][2];
+                            auto request = [&](auto GRP_, auto BUF_) {
+                                constexpr int grp = decltype(GRP_)::value, buf = decltype(BUF_)::value;
                                 if constexpr (J < NL) {
 #pragma unroll
                                     for (int k4 = 0; k4 < 4; ++k4)
                                         if (4 * grp + k4 > J) {
                                             const double2 l = *reinterpret_cast<const double2*>(
                                                 AL + ((J * NTR + 4 * grp + k4) * 32 + lsw) * 2);
-                                            lf[k4][0] = l.x;
-                                            lf[k4][1] = l.y;
+                                            lfs[buf][k4][0] = l.x;
+                                            lfs[buf][k4][1] = l.y;
                                         }
                                 } else if constexpr (J < RB) {
-                                    tm_get4(J - NL, grp, lf);
+                                    tm_ld16(tmw + (uint32_t)(((J - NL) * NTR + 4 * grp) * 4), rt[buf]);
                                 } else {
 #pragma unroll
                                     for (int k4 = 0; k4 < 4; ++k4)
                                         if (4 * grp + k4 > J) {
                                             const double2 l = *reinterpret_cast<const double2*>(lr_tile(J, 4 * grp + k4));
-                                            lf[k4][0] = l.x;
-                                            lf[k4][1] = l.y;
+                                            lfs[buf][k4][0] = l.x;
+                                            lfs[buf][k4][1] = l.y;
                                         }
+                                }
+                            };
+                            if constexpr (J >= NL && J < RB) tm_wait_st();
+                            if constexpr (G0 < NG) request(std::integral_constant<int, G0>{}, std::integral_constant<int, 0>{});
+#pragma unroll
+                            for (int grp = G0; grp < NG; ++grp) {
+                                const int buf = (grp - G0) & 1;
+                                if constexpr (J >= NL && J < RB) {   // the group's TMEM load has landed
+                                    tm_wait_ld();
+                                    tm_pin(rt[buf]);
+#pragma unroll
+                                    for (int k4 = 0; k4 < 4; ++k4) {
+                                        lfs[buf][k4][0] = u2d(rt[buf][4 * k4], rt[buf][4 * k4 + 1]);
+                                        lfs[buf][k4][1] = u2d(rt[buf][4 * k4 + 2], rt[buf][4 * k4 + 3]);
+                                    }
+                                }
+                                if (grp + 1 < NG) {
+                                    if (buf == 0) static_row<0, NG>(grp + 1, [&](auto G_) { request(G_, std::integral_constant<int, 1>{}); });
+                                    else static_row<0, NG>(grp + 1, [&](auto G_) { request(G_, std::integral_constant<int, 0>{}); });
                                 }
 #pragma unroll
                                 for (int k4 = 0; k4 < 4; ++k4)
                                     if (4 * grp + k4 > J) {
-                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lf[k4][0], b0);
-                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lf[k4][1], b1);
+                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lfs[buf][k4][0], b0);
+                                        mma884(c[4 * grp + k4][0], c[4 * grp + k4][1], lfs[buf][k4][1], b1);
                                     }
                                 if (grp == G0 && more) {   // U_{j+1,k} is final: store it, transpose it for the next step
                                     if (k < RB) home_store(J + 1, k, c[J + 1][0], c[J + 1][1]);
