@@ -482,7 +482,9 @@ def per_config_report(fp64_peak):
             out[name] = {"sweep_ms": round(m, 3), "solves_per_s": pairs / (m * 1e-3), "tflops_lu_alg": round(tf, 3),
                          "roofline_frac": round(tf / fp64_peak, 4) if fp64_peak else None,
                          "si_iterations": hist.iterations(), "si_converged": hist.converged,
-                         "si_s": round(hist.seconds, 3), "setup_s": round(setup, 2), "pairs": pairs, "n": n}
+                         "si_s": round(hist.seconds, 3), "setup_s": round(setup, 2), "pairs": pairs, "n": n,
+                         # redone calls with the pivoted kernel: 0 = the static-pivot tile LU ran throughout
+                         "pivot_fallbacks": int(L.hsw_pivot_fallbacks(s.handle))}
             s.close()
         except Exception as ex:   # report, do not lose the main line
             out[name] = {"error": str(ex)[:200]}

@@ -240,6 +240,12 @@ class SweepSolver:
         _check(L.hsw_ordering(self._h, d, None, None, _p(lag), nl.value, None, None, None))
         return SweepOrdering(order, pos, lag[: nl.value], w.value, lev)
 
+    @property
+    def pivot_fallbacks(self) -> int:
+        """Calls redone with the partial-pivoting kernel because the static-pivot tile LU refused a
+        local block (0 on the BASELINE.json configs; the handle keeps to the pivoted kernel after)."""
+        return int(_capi.load().hsw_pivot_fallbacks(self._h))
+
     def total_lagged_edges(self) -> int:
         out = C.c_int64()
         _check(_capi.load().hsw_total_lagged_edges(self._h, C.byref(out)))
