@@ -707,6 +707,7 @@ dmma2_sweep_kernel(const DevProblem pr, const double* __restrict__ src, const do
                                     // ~4 s without the other warp's column: flag it instead of hanging
                                     if (clock64() - t_wait > (1ll << 33)) {
                                         if (done_flags) atomicExch(done_flags + (size_t)pr.nel * pr.nd, 1u);
+                                        else atomicMin(err_key, (unsigned long long)pair);   // level launches: fail loudly too
                                         break;
                                     }
                                 }

@@ -1959,18 +1959,40 @@ int e2e_blocks_env() {
     }();
     return env;
 }
+// Relative block sizes of the default ramp, as cumulative 32nds (HSW_E2E_RAMP="1,4,12,24,30,32"
+// overrides: an increasing list ending in 32; its length is the block count).
+const std::vector<int>& e2e_ramp() {
+    static const std::vector<int> v = [] {
+        std::vector<int> r{0, 1, 4, 12, 24, 30, 32};
+        if (const char* e = std::getenv("HSW_E2E_RAMP")) {
+            std::vector<int> u{0};
+            for (const char* p = e; *p;) {
+                char* end = nullptr;
+                const long x = std::strtol(p, &end, 10);
+                if (end == p) break;
+                u.push_back((int)x);
+                p = *end == ',' ? end + 1 : end;
+            }
+            bool ok = u.size() >= 2 && u.back() == 32;
+            for (size_t i = 1; i < u.size(); ++i) ok = ok && u[i] > u[i - 1];
+            if (ok) r = u;
+        }
+        return r;
+    }();
+    return v;
+}
 int e2e_blocks(const hsw_handle* h, int nr) {   // nr: ordinates of the swept range
     const int env = e2e_blocks_env();
-    int b = env > 0 ? env : ((double)h->N * nr * sizeof(double) >= 64e6 ? 6 : 1);
+    int b = env > 0 ? env : ((double)h->N * nr * sizeof(double) >= 64e6 ? (int)e2e_ramp().size() - 1 : 1);
     return std::max(1, std::min(b, nr));
 }
 // First ordinate of block b (of nblk).  Default (no HSW_E2E_BLOCKS, >= 32 ordinates):
 // a ramp of relative sizes 1:3:8:12:6:2, so that only a small first block's H2D and a
 // small last block's D2H stay exposed while every other transfer hides behind a
-// larger neighbouring sweep (the copies run ~5x faster per ordinate than the sweep).
+// larger neighbouring sweep.
 int e2e_block_start(int b, int nblk, int nr) {   // offset within a range of nr ordinates
-    static const int ramp[7] = {0, 1, 4, 12, 24, 30, 32};
-    if (e2e_blocks_env() > 0 || nblk != 6 || nr < 32) return (int)((int64_t)b * nr / nblk);
+    const std::vector<int>& ramp = e2e_ramp();
+    if (e2e_blocks_env() > 0 || nblk != (int)ramp.size() - 1 || nr < 32) return (int)((int64_t)b * nr / nblk);
     return (int)((int64_t)ramp[b] * nr / 32);
 }
 
