@@ -35,6 +35,7 @@
 #include <exception>
 #include <limits>
 #include <map>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -44,6 +45,22 @@
 #include <vector>
 
 namespace hsw {
+
+// std::vector whose resize() leaves new elements uninitialised: the large tables that a
+// parallel loop fills completely are first touched by the threads that write them, not
+// zero-filled (page faults included) by one thread beforehand.
+template <typename T>
+struct default_init_allocator : std::allocator<T> {
+    template <typename U> struct rebind { using other = default_init_allocator<U>; };
+    using std::allocator<T>::allocator;
+    template <typename U> void construct(U* ptr) noexcept(std::is_nothrow_default_constructible<U>::value) {
+        ::new (static_cast<void*>(ptr)) U;
+    }
+    template <typename U, typename... Args> void construct(U* ptr, Args&&... args) {
+        ::new (static_cast<void*>(ptr)) U(std::forward<Args>(args)...);
+    }
+};
+template <typename T> using raw_vector = std::vector<T, default_init_allocator<T>>;
 
 // ------------------------------------------------------------------ threads
 static int host_workers() {
@@ -333,6 +350,18 @@ struct Mesh {
     // mesh.hpp:157-170 with a precomputed gradient table g (npe*dim) at xi
     double jacobian_tab(int e, const double* g, double* J) const {
         for (int i = 0; i < 9; ++i) J[i] = 0.0;
+        const int* en = &enodes[(size_t)e * npe];
+        if (dim == 3) {   // same sums in the same (ascending m) order, fixed trip counts
+            double j[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int m = 0; m < npe; ++m) {
+                const double* x = &pts[(size_t)en[m] * 3];
+                const double* gm = g + (size_t)m * 3;
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) j[a * 3 + b] += x[a] * gm[b];
+            }
+            for (int i = 0; i < 9; ++i) J[i] = j[i];
+            return det(J);
+        }
         for (int m = 0; m < npe; ++m) {
             const double* x = X(e, m);
             for (int a = 0; a < dim; ++a)
@@ -398,9 +427,37 @@ struct Mesh {
         return d;
     }
     // mesh.hpp:180-200 given the geometry gradient table at the face point
-    void face_geometry_tab(int e, int f, const double* g, double* normal, double& sj) const {
+    // diam: the element's diameter when the caller already has it (< 0: computed here)
+    // Jacobians of element e at n points at once: gt is the gradient table transposed to
+    // [npe][n * dim] (point-major inside a node), out is [dim][n * dim], so that
+    // J_q[a][b] = out[a * n * dim + q * dim + b].  Every entry is the same sum over the
+    // nodes in the same ascending order as jacobian_tab (no FMA contraction), so the bits
+    // agree; the inner loop runs over contiguous memory and vectorises.
+    void jacobians_batch(int e, const double* gt, int n, double* out) const {
+        const int w = n * dim;
+        for (int i = 0; i < dim * w; ++i) out[i] = 0.0;
+        const int* en = &enodes[(size_t)e * npe];
+        for (int m = 0; m < npe; ++m) {
+            const double* x = &pts[(size_t)en[m] * dim];
+            const double* gm = gt + (size_t)m * w;
+            for (int a = 0; a < dim; ++a) {
+                const double xa = x[a];
+                double* o = out + (size_t)a * w;
+                for (int i = 0; i < w; ++i) o[i] += xa * gm[i];
+            }
+        }
+    }
+    void unpack_jacobian(const double* out, int n, int q, double* J) const {
+        for (int i = 0; i < 9; ++i) J[i] = 0.0;
+        for (int a = 0; a < dim; ++a)
+            for (int b = 0; b < dim; ++b) J[a * 3 + b] = out[(size_t)a * n * dim + (size_t)q * dim + b];
+    }
+    void face_geometry_tab(int e, int f, const double* g, double* normal, double& sj, double diam = -1.0) const {
         double J[9];
         jacobian_tab(e, g, J);
+        face_geometry_J(e, f, J, normal, sj, diam);
+    }
+    void face_geometry_J(int e, int f, const double* J, double* normal, double& sj, double diam = -1.0) const {
         int a0, a1;
         face_axes(dim, f, a0, a1);
         if (dim == 2) {
@@ -414,7 +471,7 @@ struct Mesh {
             const double c2 = u0 * v1 - u1 * v0;
             sj = std::sqrt(c0 * c0 + c1 * c1 + c2 * c2);
         }
-        if (sj < 1e-14 * diameter(e))
+        if (sj < 1e-14 * (diam >= 0.0 ? diam : diameter(e)))
             throw Error(HSW_ERR_GEOMETRY, "face_geometry: degenerate tangent on element " +
                                               std::to_string(e) + " face " + std::to_string(f));
         double K[9], nref[3];
@@ -737,19 +794,33 @@ static Ordering sweep_ordering(int n, const std::vector<Edge>& edges, int thr) {
     const std::vector<int>& comp = S.comp;
     const int nc = (int)S.off.size() - 1;
     // condensation edges, sorted unique per source component (CSR)
+    // (bucketed by source component, each small bucket sorted and deduplicated: the same
+    // list as a global sort + unique of the (source, target) pairs)
     std::vector<std::pair<int, int>> ce;
-    for (const auto& e : edges) {
-        const int cu = comp[e.from], cv = comp[e.to];
-        if (cu != cv) ce.push_back({cu, cv});
-    }
-    std::sort(ce.begin(), ce.end());
-    ce.erase(std::unique(ce.begin(), ce.end()), ce.end());
     std::vector<int> coff((size_t)nc + 1, 0), cin(nc, 0);
-    for (const auto& pr : ce) {
-        coff[(size_t)pr.first + 1]++;
-        cin[pr.second]++;
+    {
+        std::vector<int> boff((size_t)nc + 1, 0);
+        for (const auto& e : edges)
+            if (comp[e.from] != comp[e.to]) boff[(size_t)comp[e.from] + 1]++;
+        for (int c = 0; c < nc; ++c) boff[(size_t)c + 1] += boff[c];
+        std::vector<int> tgt(boff[nc]), fill(boff.begin(), boff.end() - 1);
+        for (const auto& e : edges) {
+            const int cu = comp[e.from], cv = comp[e.to];
+            if (cu != cv) tgt[fill[cu]++] = cv;
+        }
+        ce.reserve(tgt.size());
+        for (int c = 0; c < nc; ++c) {
+            int* b = tgt.data() + boff[c];
+            int* e = tgt.data() + boff[(size_t)c + 1];
+            std::sort(b, e);
+            e = std::unique(b, e);
+            for (int* q = b; q != e; ++q) {
+                ce.push_back({c, *q});
+                cin[*q]++;
+            }
+            coff[(size_t)c + 1] = (int)ce.size();
+        }
     }
-    for (int c = 0; c < nc; ++c) coff[(size_t)c + 1] += coff[c];
     using Key = std::pair<int, int>;
     std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
     for (int c = 0; c < nc; ++c)
@@ -922,8 +993,8 @@ struct Setup {
     // per element
     std::vector<double> T;      // E*nb*nb*4
     std::vector<double> sig_t, sig_s, qvol;  // E, E, E*nb
-    std::vector<double> fgeom;  // E*nf*nqf*4 (normal, w*sj)
-    std::vector<double> fsj;    // E*nf*nqf   (sj)
+    raw_vector<double> fgeom;  // E*nf*nqf*4 (normal, w*sj)
+    raw_vector<double> fsj;    // E*nf*nqf   (sj)
     std::vector<int> fnbr;      // E*nf*4
     std::vector<int> bface_of;  // E*nf -> boundary face id or -1
     // face trace tables (bit-exact with the reference element-wise arithmetic)
@@ -931,7 +1002,8 @@ struct Setup {
     std::vector<std::vector<double>> traceR;  // per orientation code: nqf * nfn at mapped point
     // max|LR|, max|RL| per (ordinate, interior face) computed on the device
     // (hsw_setup.cu, bit-identical to the host loop below); empty: host computes
-    std::vector<double> dev_cmax;
+    std::unique_ptr<double[]> dev_cmax;   // uninitialised storage: the device copy overwrites all of it
+    std::function<void(int)> cmax_wait;   // blocks until ordinate d's block of dev_cmax has arrived
     // per ordinate
     std::vector<std::vector<Coupling>> couplings;
     std::vector<std::vector<double>> weights;
@@ -941,7 +1013,7 @@ struct Setup {
     // worklists
     int num_levels = 0;
     std::vector<int> level_offsets;  // num_levels+1 into pairs_all
-    std::vector<int> pairs_all;      // e*nd + d, sorted (level, e, d)
+    raw_vector<int> pairs_all;      // e*nd + d, sorted (level, e, d)
     std::vector<std::vector<int>> dir_level_offsets;  // per d
     std::vector<int> pairs_dir;      // per d block of E pairs sorted by level
     std::vector<int> face_id_of;     // E*nf -> interior face id or -1
@@ -1061,8 +1133,12 @@ struct Setup {
     }
 
     void build_mesh(int num_points, bool validate) {
+        auto T0 = std::chrono::steady_clock::now();
+        auto TT = [&](const char* n) { if (std::getenv("HSW_SETUP_TIMING")) { auto t = std::chrono::steady_clock::now(); std::fprintf(stderr, "  bm %s %.3f\n", n, std::chrono::duration<double>(t - T0).count()); T0 = t; } };
         mesh.check_connectivity(num_points);
+        TT("check");
         mesh.build_faces();
+        TT("build_faces");
         face_id_of.assign((size_t)nel * nf, -1);
         bface_of.assign((size_t)nel * nf, -1);
         fnbr.assign((size_t)nel * nf * 4, -1);
@@ -1081,51 +1157,74 @@ struct Setup {
             int* a = &fnbr[((size_t)B.elem * nf + B.face) * 4];
             a[0] = -1; a[1] = -1; a[2] = 0; a[3] = (int)i;
         }
+        TT("fnbr");
         if (validate) {
             // mesh.hpp:219-228 det(J) > 0 on an (order+2)^dim lattice
             const int ns = mesh.order + 2;
             const int nz = dim == 3 ? ns : 1;
-            std::vector<std::vector<double>> gtab;
-            for (int k = 0; k < nz; ++k)
-                for (int j = 0; j < ns; ++j)
-                    for (int i = 0; i < ns; ++i) {
-                        const double xi[3] = {i / double(ns - 1), j / double(ns - 1), dim == 3 ? k / double(ns - 1) : 0.0};
-                        std::vector<double> g((size_t)mesh.npe * dim);
-                        mesh.geom.gradients(xi, g.data());
-                        gtab.push_back(std::move(g));
-                    }
+            const int nlat = ns * ns * nz;
+            std::vector<double> gtab((size_t)mesh.npe * nlat * dim);   // [npe][nlat * dim]
+            {
+                std::vector<double> g((size_t)mesh.npe * dim);
+                int q = 0;
+                for (int k = 0; k < nz; ++k)
+                    for (int j = 0; j < ns; ++j)
+                        for (int i = 0; i < ns; ++i, ++q) {
+                            const double xi[3] = {i / double(ns - 1), j / double(ns - 1),
+                                                  dim == 3 ? k / double(ns - 1) : 0.0};
+                            mesh.geom.gradients(xi, g.data());
+                            for (int m = 0; m < mesh.npe; ++m)
+                                for (int b = 0; b < dim; ++b)
+                                    gtab[((size_t)m * nlat + q) * dim + b] = g[(size_t)m * dim + b];
+                        }
+            }
             std::atomic<int> bad{std::numeric_limits<int>::max()};
             parallel_for(nel, [&](int64_t e) {
+                thread_local std::vector<double> jb;
+                jb.resize((size_t)dim * nlat * dim);
+                mesh.jacobians_batch((int)e, gtab.data(), nlat, jb.data());
                 double J[9];
-                for (const auto& g : gtab)
-                    if (mesh.jacobian_tab((int)e, g.data(), J) <= 0.0) {
+                for (int q = 0; q < nlat; ++q) {
+                    mesh.unpack_jacobian(jb.data(), nlat, q, J);
+                    if (mesh.det(J) <= 0.0) {
                         int cur = bad.load();
                         while ((int)e < cur && !bad.compare_exchange_weak(cur, (int)e)) {}
                         return;
                     }
+                }
             });
             if (bad.load() != std::numeric_limits<int>::max())
                 throw Error(HSW_ERR_MESH, "mesh: element " + std::to_string(bad.load()) + " has non-positive Jacobian");
+            TT("detJ");
             // mesh.hpp:346-365 trace agreement on a 5-point (5x5) lattice
             std::atomic<int64_t> badf{std::numeric_limits<int64_t>::max()};
-            parallel_for((int64_t)mesh.ifaces.size(), [&](int64_t i) {
-                thread_local std::vector<double> v, vr;
-                v.resize((size_t)mesh.npe);
-                vr.resize((size_t)mesh.npe);
-                const auto& F = mesh.ifaces[i];
-                const double tol = 1e-12 * mesh.diameter(F.el);
-                const int nt = dim == 3 ? 5 : 1;
+            // geometry basis values at the lattice points, tabulated per (face, lattice point)
+            // on the left and per (face, orientation, lattice point) on the right
+            const int nt = dim == 3 ? 5 : 1, nlp = 5 * nt, ncodes = dim == 2 ? 2 : 8;
+            const size_t npe = (size_t)mesh.npe;
+            std::vector<double> vl((size_t)nf * nlp * npe), vrt((size_t)nf * ncodes * nlp * npe);
+            for (int f = 0; f < nf; ++f)
                 for (int kt = 0; kt < nt; ++kt)
                     for (int k = 0; k < 5; ++k) {
                         const double s = k / 4.0, t = dim == 3 ? kt / 4.0 : 0.0;
-                        double so, to, xil[3], xir[3], xl[3], xr[3];
-                        orient_param(dim, F.orient, s, t, so, to);
-                        param_point(dim, F.fl, s, t, xil);
-                        param_point(dim, F.fr, so, to, xir);
-                        mesh.geom.values(xil, v.data());
-                        mesh.geom.values(xir, vr.data());
-                        mesh.map_tab(F.el, v.data(), xl);
-                        mesh.map_tab(F.er, vr.data(), xr);
+                        double xi[3];
+                        param_point(dim, f, s, t, xi);
+                        mesh.geom.values(xi, &vl[((size_t)f * nlp + kt * 5 + k) * npe]);
+                        for (int c = 0; c < ncodes; ++c) {
+                            double so, to;
+                            orient_param(dim, c, s, t, so, to);
+                            param_point(dim, f, so, to, xi);
+                            mesh.geom.values(xi, &vrt[(((size_t)f * ncodes + c) * nlp + kt * 5 + k) * npe]);
+                        }
+                    }
+            parallel_for((int64_t)mesh.ifaces.size(), [&](int64_t i) {
+                const auto& F = mesh.ifaces[i];
+                const double tol = 1e-12 * mesh.diameter(F.el);
+                for (int kt = 0; kt < nt; ++kt)
+                    for (int k = 0; k < 5; ++k) {
+                        double xl[3], xr[3];
+                        mesh.map_tab(F.el, &vl[((size_t)F.fl * nlp + kt * 5 + k) * npe], xl);
+                        mesh.map_tab(F.er, &vrt[(((size_t)F.fr * ncodes + F.orient) * nlp + kt * 5 + k) * npe], xr);
                         double d2 = 0.0;
                         for (int a = 0; a < dim; ++a) d2 += (xl[a] - xr[a]) * (xl[a] - xr[a]);
                         if (std::sqrt(d2) > tol) {   // the lowest failing face is reported
@@ -1141,6 +1240,7 @@ struct Setup {
                                               " traces disagree between elements " + std::to_string(F.el) +
                                               " and " + std::to_string(F.er));
             }
+            TT("traces");
         }
     }
 
@@ -1235,28 +1335,41 @@ struct Setup {
 
     // per element face geometry (own side) + trace tables
     void face_tables() {
-        std::vector<std::vector<double>> GGf(nf);  // per face: nqf * npe * dim gradient tables
-        for (int f = 0; f < nf; ++f) {
-            GGf[f].resize((size_t)nqf * mesh.npe * dim);
-            for (int q = 0; q < nqf; ++q) {
-                double xi[3];
-                param_point(dim, f, fq_pts[q][0], fq_pts[q][1], xi);
-                mesh.geom.gradients(xi, &GGf[f][(size_t)q * mesh.npe * dim]);
+        // per face: gradient tables at the face points, transposed to [npe][nqf * dim]
+        std::vector<std::vector<double>> GGf(nf);
+        {
+            std::vector<double> g((size_t)mesh.npe * dim);
+            for (int f = 0; f < nf; ++f) {
+                GGf[f].resize((size_t)nqf * mesh.npe * dim);
+                for (int q = 0; q < nqf; ++q) {
+                    double xi[3];
+                    param_point(dim, f, fq_pts[q][0], fq_pts[q][1], xi);
+                    mesh.geom.gradients(xi, g.data());
+                    for (int m = 0; m < mesh.npe; ++m)
+                        for (int b = 0; b < dim; ++b)
+                            GGf[f][((size_t)m * nqf + q) * dim + b] = g[(size_t)m * dim + b];
+                }
             }
         }
-        fgeom.assign((size_t)nel * nf * nqf * 4, 0.0);
-        fsj.assign((size_t)nel * nf * nqf, 0.0);
+        fgeom.resize((size_t)nel * nf * nqf * 4);   // every entry is written below
+        fsj.resize((size_t)nel * nf * nqf);
         parallel_for(nel, [&](int64_t e64) {
             const int e = (int)e64;
-            for (int f = 0; f < nf; ++f)
+            const double diam = mesh.diameter(e);
+            thread_local std::vector<double> jb;
+            jb.resize((size_t)dim * nqf * dim);
+            for (int f = 0; f < nf; ++f) {
+                mesh.jacobians_batch(e, GGf[f].data(), nqf, jb.data());
                 for (int q = 0; q < nqf; ++q) {
-                    double n[3], sj;
-                    mesh.face_geometry_tab(e, f, &GGf[f][(size_t)q * mesh.npe * dim], n, sj);
+                    double n[3], sj, J[9];
+                    mesh.unpack_jacobian(jb.data(), nqf, q, J);
+                    mesh.face_geometry_J(e, f, J, n, sj, diam);
                     double* g = &fgeom[(((size_t)e * nf + f) * nqf + q) * 4];
                     g[0] = n[0]; g[1] = n[1]; g[2] = n[2];
                     g[3] = fq_w[q] * sj;
                     fsj[((size_t)e * nf + f) * nqf + q] = sj;
                 }
+            }
         });
         // traces: full basis values at the face param point, face nodes picked
         // (assembly.hpp:112-116); identical for every face (one factor is exactly 1).
@@ -1311,6 +1424,9 @@ struct Setup {
             std::vector<double> LR((size_t)nfn * nfn), RL((size_t)nfn * nfn), wp(nqf), wm(nqf);
             auto& cpl = couplings[d];
             auto& wts = weights[d];
+            cpl.reserve((size_t)nfi + nfi / 8);   // about one coupling per interior face
+            wts.reserve((size_t)nfi + nfi / 8);
+            if (dev_cmax && cmax_wait) cmax_wait(d);
             // Romberg sampling of one face at parameter t (assembly.hpp:103-117): geometry of
             // the (left) element's face, its face-node traces, the neighbour's at t or 1 - t
             std::vector<double> gg((size_t)mesh.npe * dim), full(nb), ul(nfn), ur(nfn), packed, gtmp;
@@ -1408,7 +1524,7 @@ struct Setup {
                 std::fill(RL.begin(), RL.end(), 0.0);
                 double length = 0.0;
                 const double* uR0 = traceR[F.orient].data();
-                if (!dev_cmax.empty()) {   // magnitudes from the device; length here
+                if (dev_cmax) {   // magnitudes from the device; length here
                     double length = 0.0;
                     for (int q = 0; q < nqf; ++q) length += fq_w[q] * sjv[q];
                     const double eps = 1e-12 * length;
@@ -1545,34 +1661,58 @@ struct Setup {
     }
 
     void worklists() {   // over the handle's ordinate shard [ob, oe)
-        int maxl = 0;
-        for (int d = ob; d < oe; ++d)
-            for (int e = 0; e < nel; ++e) maxl = std::max(maxl, ords[d].level[e]);
-        num_levels = maxl + 1;
-        // shard worklist sorted by (level, element, ordinate)
-        std::vector<int> count(num_levels + 1, 0);
-        for (int e = 0; e < nel; ++e)
-            for (int d = ob; d < oe; ++d) count[ords[d].level[e] + 1]++;
-        for (int l = 0; l < num_levels; ++l) count[l + 1] += count[l];
-        level_offsets = count;
-        pairs_all.assign((size_t)nel * (oe - ob), 0);
-        std::vector<int> fill(count.begin(), count.end() - 1);
-        for (int e = 0; e < nel; ++e)
-            for (int d = ob; d < oe; ++d) pairs_all[fill[ords[d].level[e]]++] = e * nd + d;
-        // per-ordinate worklists
-        pairs_dir.assign((size_t)nel * nd, 0);
+        const int nds = oe - ob;
+        // per-ordinate worklists (level, element) and level counts, one ordinate per task
+        pairs_dir.resize((size_t)nel * nd);
+        if (nds < nd) std::fill(pairs_dir.begin(), pairs_dir.end(), 0);   // rows outside the shard
         dir_level_offsets.assign(nd, {});
-        for (int d = ob; d < oe; ++d) {
+        parallel_for(nds, [&](int64_t i) {
+            const int d = ob + (int)i;
+            const int* lev = ords[d].level.data();
             int ml = 0;
-            for (int e = 0; e < nel; ++e) ml = std::max(ml, ords[d].level[e]);
+            for (int e = 0; e < nel; ++e) ml = std::max(ml, lev[e]);
             std::vector<int> c(ml + 2, 0);
-            for (int e = 0; e < nel; ++e) c[ords[d].level[e] + 1]++;
+            for (int e = 0; e < nel; ++e) c[lev[e] + 1]++;
             for (int l = 0; l <= ml; ++l) c[l + 1] += c[l];
-            dir_level_offsets[d] = c;
             std::vector<int> fl(c.begin(), c.end() - 1);
             int* base = &pairs_dir[(size_t)d * nel];
-            for (int e = 0; e < nel; ++e) base[fl[ords[d].level[e]]++] = e * nd + d;
+            for (int e = 0; e < nel; ++e) base[fl[lev[e]]++] = e * nd + d;
+            dir_level_offsets[d] = std::move(c);
+        });
+        int maxl = 0;
+        for (int d = ob; d < oe; ++d) maxl = std::max(maxl, (int)dir_level_offsets[d].size() - 2);
+        num_levels = maxl + 1;
+        // shard worklist sorted by (level, element, ordinate): element chunks count their
+        // pairs per level, a prefix over (level, chunk) gives every chunk its write offsets
+        const int nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(nel, 4 * (int64_t)host_workers()));
+        auto chunk_begin = [&](int k) { return (int)((int64_t)nel * k / nchunk); };
+        std::vector<int> cnt((size_t)nchunk * num_levels, 0);
+        parallel_for(nchunk, [&](int64_t k) {
+            int* c = &cnt[(size_t)k * num_levels];
+            for (int d = ob; d < oe; ++d) {
+                const int* lev = ords[d].level.data();
+                for (int e = chunk_begin((int)k); e < chunk_begin((int)k + 1); ++e) c[lev[e]]++;
+            }
+        });
+        level_offsets.assign(num_levels + 1, 0);
+        {
+            int run = 0;
+            for (int l = 0; l < num_levels; ++l) {
+                level_offsets[l] = run;
+                for (int k = 0; k < nchunk; ++k) {
+                    const int c = cnt[(size_t)k * num_levels + l];
+                    cnt[(size_t)k * num_levels + l] = run;
+                    run += c;
+                }
+            }
+            level_offsets[num_levels] = run;
         }
+        pairs_all.resize((size_t)nel * nds);
+        parallel_for(nchunk, [&](int64_t k) {
+            int* fill = &cnt[(size_t)k * num_levels];
+            for (int e = chunk_begin((int)k); e < chunk_begin((int)k + 1); ++e)
+                for (int d = ob; d < oe; ++d) pairs_all[fill[ords[d].level[e]]++] = e * nd + d;
+        });
     }
 };
 
@@ -1655,6 +1795,30 @@ struct hsw_handle {
 };
 
 namespace {
+// fn on a helper thread; join() rethrows what it threw (the destructor only joins)
+struct Async {
+    std::exception_ptr err;
+    std::thread t;
+    template <class F>
+    explicit Async(F&& f) : t([this, fn = std::forward<F>(f)]() mutable {
+        try {
+            fn();
+        } catch (...) {
+            err = std::current_exception();
+        }
+    }) {}
+    void join() {
+        if (t.joinable()) t.join();
+        if (err) {
+            std::exception_ptr e = err;
+            err = nullptr;
+            std::rethrow_exception(e);
+        }
+    }
+    ~Async() {
+        if (t.joinable()) t.join();
+    }
+};
 thread_local std::string g_last_error;
 thread_local int g_create_zero_e = -1, g_create_zero_d = -1;
 
@@ -1685,8 +1849,8 @@ int fail(int status, const std::string& msg) {
                                                " at " #x);                                   \
     } while (0)
 
-template <typename T>
-T* dev_upload(const std::vector<T>& v) {
+template <typename T, typename A>
+T* dev_upload(const std::vector<T, A>& v) {
     T* p = nullptr;
     if (v.empty()) return nullptr;
     CUDA_OK(cudaMalloc(&p, v.size() * sizeof(T)));
@@ -2145,42 +2309,99 @@ void device_init(hsw_handle* h, int device) {
 }
 
 // max|LR|, max|RL| of every (ordinate, interior face) on the device, in blocks
-// of ordinates, into S.dev_cmax for Setup::ordinates
-void device_coupling_max(hsw_handle* h) {
-    Setup& S = h->S;
-    const int nfi = (int)S.mesh.ifaces.size();
-    S.dev_cmax.assign((size_t)(S.oe - S.ob) * nfi * 2, 0.0);
-    if (nfi == 0) return;
-    std::vector<int> iface((size_t)nfi * 5);
-    for (int i = 0; i < nfi; ++i) {
-        const IFace& F = S.mesh.ifaces[i];
-        int* r = &iface[(size_t)i * 5];
-        r[0] = F.el; r[1] = F.er; r[2] = F.fl; r[3] = F.fr; r[4] = F.orient;
+// of ordinates, into S.dev_cmax for Setup::ordinates.  The blocks
+// are produced on a helper thread in ascending ordinate order while Setup::ordinates
+// (whose tasks are claimed in the same order) already works on the finished ones:
+// S.cmax_wait(d) blocks until ordinate d's magnitudes have arrived.
+struct CouplingFeed {
+    hsw_handle* h;
+    int nfi = 0, chunk = 1, nchunks = 0;
+    int* d_if = nullptr;
+    double *d_sj = nullptr, *d_w = nullptr, *d_tr = nullptr, *d_trR = nullptr, *d_od = nullptr;
+    double* d_out[2] = {nullptr, nullptr};
+    cudaStream_t kern = nullptr, copy = nullptr;   // its own streams: the handle's stream builds device state meanwhile
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    std::unique_ptr<std::atomic<int>[]> ready;
+    std::atomic<bool> failed{false};
+
+    explicit CouplingFeed(hsw_handle* hh) : h(hh) {
+        Setup& S = h->S;
+        nfi = (int)S.mesh.ifaces.size();
+        if (nfi == 0) return;
+        S.dev_cmax.reset(new double[(size_t)(S.oe - S.ob) * nfi * 2]);
+        std::vector<int> iface((size_t)nfi * 5);
+        for (int i = 0; i < nfi; ++i) {
+            const IFace& F = S.mesh.ifaces[i];
+            int* r = &iface[(size_t)i * 5];
+            r[0] = F.el; r[1] = F.er; r[2] = F.fl; r[3] = F.fr; r[4] = F.orient;
+        }
+        std::vector<double> trR;
+        for (const auto& t : S.traceR) trR.insert(trR.end(), t.begin(), t.end());
+        d_if = dev_upload(iface);
+        h->d_fgeom = dev_upload(S.fgeom);   // kept: the sweep kernels' face geometry
+        d_sj = dev_upload(S.fsj);
+        d_w = dev_upload(S.fq_w);
+        d_tr = dev_upload(S.trace);
+        d_trR = dev_upload(trR);
+        d_od = dev_upload(S.odir);
+        // blocks of about 24 MB of magnitudes (C4: 16 ordinates), two device buffers
+        chunk = std::max(1, std::min(S.oe - S.ob, (int)(std::max<size_t>(1, (size_t)(24u << 20) / ((size_t)nfi * 16)))));
+        nchunks = (S.oe - S.ob + chunk - 1) / chunk;
+        for (auto& b : d_out) CUDA_OK(cudaMalloc(&b, (size_t)chunk * nfi * 2 * sizeof(double)));
+        CUDA_OK(cudaStreamCreateWithFlags(&kern, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        for (auto& e : ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ready.reset(new std::atomic<int>[nchunks]);
+        for (int k = 0; k < nchunks; ++k) ready[k].store(0);
+        S.cmax_wait = [this](int d) {
+            const int k = (d - h->S.ob) / chunk;
+            while (!ready[k].load(std::memory_order_acquire)) {
+                if (failed.load()) throw hsw::Error(HSW_ERR_CUDA, "hsw_create: the device coupling pass failed");
+                std::this_thread::sleep_for(std::chrono::microseconds(50));
+            }
+        };
     }
-    std::vector<double> trR;
-    for (const auto& t : S.traceR) trR.insert(trR.end(), t.begin(), t.end());
-    int* d_if = dev_upload(iface);
-    double* d_geo = dev_upload(S.fgeom);
-    double* d_sj = dev_upload(S.fsj);
-    double* d_w = dev_upload(S.fq_w);
-    double* d_tr = dev_upload(S.trace);
-    double* d_trR = dev_upload(trR);
-    double* d_od = dev_upload(S.odir);
-    const int chunk = std::max(1, std::min(S.nd, (int)(std::max<size_t>(1, (size_t)(256u << 20) / ((size_t)nfi * 16)))));
-    double* d_out = nullptr;
-    CUDA_OK(cudaMalloc(&d_out, (size_t)chunk * nfi * 2 * sizeof(double)));
-    for (int d0 = S.ob; d0 < S.oe; d0 += chunk) {
-        const int d1 = std::min(S.oe, d0 + chunk);
-        dev_coupling_max(S.dim, nfi, S.nf, S.nqf, S.nfn, d_if, d_geo, d_sj, d_w, d_tr, d_trR, d_od, d0, d1, d_out,
-                         h->stream);
-        CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)(d0 - S.ob) * nfi * 2], d_out,
-                                (size_t)(d1 - d0) * nfi * 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    void launch(int k) {
+        Setup& S = h->S;
+        const int d0 = S.ob + k * chunk, d1 = std::min(S.oe, d0 + chunk);
+        dev_coupling_max(S.dim, nfi, S.nf, S.nqf, S.nfn, d_if, h->d_fgeom, d_sj, d_w, d_tr, d_trR, d_od, d0, d1,
+                         d_out[k & 1], kern);
+        CUDA_OK(cudaEventRecord(ev[k & 1], kern));
     }
-    CUDA_OK(cudaStreamSynchronize(h->stream));
-    for (void* b : {(void*)d_if, (void*)d_geo, (void*)d_sj, (void*)d_w, (void*)d_tr, (void*)d_trR, (void*)d_od,
-                    (void*)d_out})
-        cudaFree(b);
-}
+    void produce() {   // helper thread
+        if (nfi == 0) return;
+        try {
+            Setup& S = h->S;
+            CUDA_OK(cudaSetDevice(h->device));
+            launch(0);
+            for (int k = 0; k < nchunks; ++k) {
+                // block k + 1 is computed while block k is copied (its buffer was drained
+                // by the synchronous copy of block k - 1)
+                if (k + 1 < nchunks) launch(k + 1);
+                const int d0 = S.ob + k * chunk, d1 = std::min(S.oe, d0 + chunk);
+                CUDA_OK(cudaStreamWaitEvent(copy, ev[k & 1], 0));
+                CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)(d0 - S.ob) * nfi * 2], d_out[k & 1],
+                                        (size_t)(d1 - d0) * nfi * 2 * sizeof(double), cudaMemcpyDeviceToHost, copy));
+                CUDA_OK(cudaStreamSynchronize(copy));
+                ready[k].store(1, std::memory_order_release);
+            }
+        } catch (...) {
+            failed.store(true);
+            throw;
+        }
+    }
+    ~CouplingFeed() {
+        h->S.cmax_wait = nullptr;
+        if (kern) cudaStreamSynchronize(kern);
+        for (void* b : {(void*)d_if, (void*)d_sj, (void*)d_w, (void*)d_tr, (void*)d_trR, (void*)d_od, (void*)d_out[0],
+                        (void*)d_out[1]})
+            cudaFree(b);
+        if (kern) cudaStreamDestroy(kern);
+        if (copy) cudaStreamDestroy(copy);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
 }  // namespace
 
 int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
@@ -2200,34 +2421,43 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         };
         S.ingest(desc);
         phase("ingest");
-        S.build_mesh(desc->num_points, desc->validate_geometry != 0);
-        phase("build_mesh");
+        {   // the face geometry tables need the points and the (checked) connectivity only:
+            // they are filled beside the face pairing / geometry validation of build_mesh
+            S.mesh.check_connectivity(desc->num_points);
+            Async faces([&] {
+                const auto t0 = std::chrono::steady_clock::now();
+                S.face_tables();
+                if (timing)
+                    std::fprintf(stderr, "  (face_tables, beside build_mesh) %.3f s\n",
+                                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+            });
+            S.build_mesh(desc->num_points, desc->validate_geometry != 0);
+            faces.join();
+        }
+        phase("mesh+face_tables");
         // element tensors on the device unless host-only, or the siginvface weights
         // need the host's exact M_t arithmetic (sweepgraph.hpp:65-72)
         const bool host_T = desc->device < 0 || S.weighting == HSW_WEIGHT_SIGINVFACE;
         S.element_tensors(host_T);
         phase("element_tensors");
-        S.face_tables();
-        phase("face_tables");
         if (desc->device >= 0) {
             device_init(h, desc->device);
             if (S.dim == 3 && S.face_pts != S.p + 2)
                 throw hsw::Error(HSW_ERR_INVALID, "hsw_create: the 3D kernels integrate faces with p + 2 Gauss "
                                                   "points per axis (face_points " + std::to_string(S.face_pts) + ")");
-            if (S.weighting != HSW_WEIGHT_SIGINVFACE && !S.face_blocks()) {
-                // (siginvface needs the blocks on the host; Romberg integrates them there)
-                device_coupling_max(h);
-                phase("couplings(dev)");
-            }
         }
-        S.ordinates();
-        phase("ordinates");
-        S.worklists();
-        phase("worklists");
-        // device (device < 0: host-only plan, used by the CPU tests of the host logic)
-        if (desc->device < 0) return HSW_OK;
-        S.dev_cmax.clear();
-        S.dev_cmax.shrink_to_fit();
+        if (desc->device < 0) {   // host-only plan, used by the CPU tests of the host logic
+            S.ordinates();
+            phase("ordinates");
+            S.worklists();
+            phase("worklists");
+            return HSW_OK;
+        }
+        // Device state that does not depend on the orderings (tables, element tensors, materials,
+        // psi / phi buffers) is built on a helper thread while the host works through the
+        // per-ordinate graphs; the plan-dependent arrays are uploaded after both are done.
+        auto device_static = [&] {
+        CUDA_OK(cudaSetDevice(h->device));
         ConstTables ct{};
         for (int f = 0; f < S.nf; ++f)
             for (int a = 0; a < S.nfn; ++a) ct.fnode[f][a] = S.fnodes[f][a];
@@ -2302,16 +2532,13 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         h->d_sig_s = dev_upload(S.sig_s);
         CUDA_OK(cudaMalloc(&h->d_bscale, (size_t)S.nel * sizeof(double)));
         dev_block_scale(S.nel, S.nb, h->d_T, h->d_sig_t, h->d_bscale, h->stream);
-        h->d_fgeom = dev_upload(S.fgeom);
+        if (!h->d_fgeom) h->d_fgeom = dev_upload(S.fgeom);
         h->d_fnbr = dev_upload(S.fnbr);
-        h->d_inflags = dev_upload(S.inflags);
         std::vector<double> om((size_t)S.nd * 4, 0.0);
         for (int d = 0; d < S.nd; ++d)
             for (int k = 0; k < 3; ++k) om[(size_t)d * 4 + k] = k < S.dim ? S.odir[3 * d + k] : 0.0;
         h->d_omega = dev_upload(om);
         h->d_weight = dev_upload(S.ow);
-        h->d_pairs_all = dev_upload(S.pairs_all);
-        h->d_pairs_dir = dev_upload(S.pairs_dir);
         h->N = (size_t)S.nel * S.nb;
         // psi of the shard's ordinates only; the handle's pointers are offset so that row d of
         // the global [nd][N] layout addresses ordinate d (kernels index psi by global d)
@@ -2338,6 +2565,26 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
         CUDA_OK(cudaMemset(h->d_prof, 0, 16 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemset(h->d_err, 0xff, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMallocHost(&h->h_out, 8 * sizeof(double)));
+        };   // device_static
+        {
+            // (siginvface needs the coupling blocks on the host; Romberg integrates them there)
+            const bool dev_cpl = S.weighting != HSW_WEIGHT_SIGINVFACE && !S.face_blocks();
+            std::unique_ptr<CouplingFeed> feed(dev_cpl ? new CouplingFeed(h) : nullptr);
+            phase("coupling uploads");
+            Async cpl([&] { if (feed) feed->produce(); });
+            Async dev(device_static);
+            S.ordinates();
+            phase("ordinates");
+            S.worklists();
+            phase("worklists");
+            cpl.join();
+            dev.join();
+            phase("device state");
+        }
+        S.dev_cmax.reset();
+        h->d_inflags = dev_upload(S.inflags);
+        h->d_pairs_all = dev_upload(S.pairs_all);
+        h->d_pairs_dir = dev_upload(S.pairs_dir);
         DevProblem& P = h->P;
         P.dim = S.dim; P.p = S.p; P.nb = S.nb; P.nfn = S.nfn; P.nqf = S.nqf; P.nfaces = S.nf;
         P.nel = S.nel; P.nd = S.nd;

@@ -308,25 +308,34 @@ coupling_max_kernel(int dim, int nfi, int nf, int nqf, int nfn, const int* __res
     const double* uR = traceR + (size_t)orient * nqf * nfn;
     for (int d = d0; d < d1; ++d) {
         __syncthreads();   // s_wm / s_wp reuse
+        int any_p = 0, any_m = 0;
         for (int q = threadIdx.x; q < nqf; q += kCplThreads) {
             double on = 0.0;
             for (int k = 0; k < dim; ++k) on = __dadd_rn(on, __dmul_rn(odir[d * 3 + k], s_geo[q * 4 + k]));
             s_wp[q] = __dmul_rn(0.5, __dadd_rn(on, fabs(on)));
             s_wm[q] = __dmul_rn(0.5, __dadd_rn(fabs(on), -on));
+            any_p |= s_wp[q] != 0.0;
+            any_m |= s_wm[q] != 0.0;
         }
-        __syncthreads();
+        // a face the ordinate crosses one way only has w- == 0 (or w+ == 0) at every point: that
+        // block is a sum of zero products, |.| = 0 exactly, and is skipped (as the host does)
+        const bool do_lr = __syncthreads_or(any_m) != 0;
+        const bool do_rl = __syncthreads_or(any_p) != 0;
         double mlr = 0.0, mrl = 0.0;
         for (int mn = threadIdx.x; mn < nfn * nfn; mn += kCplThreads) {
             const int m = mn / nfn, n = mn - m * nfn;
             double lr = 0.0, rl = 0.0;
-            for (int q = 0; q < nqf; ++q) {
-                const double w = fqw[q], sj = s_sj[q];
-                const double ul_m = trace[q * nfn + m], ur_n = uR[q * nfn + n];
-                const double ur_m = uR[q * nfn + m], ul_n = trace[q * nfn + n];
-                // row[n] += w * (c * ur[n] * sj), c = w- * ul[m]   (and the mirrored RL term)
-                lr = __dadd_rn(lr, __dmul_rn(w, __dmul_rn(__dmul_rn(__dmul_rn(s_wm[q], ul_m), ur_n), sj)));
-                rl = __dadd_rn(rl, __dmul_rn(w, __dmul_rn(__dmul_rn(__dmul_rn(s_wp[q], ur_m), ul_n), sj)));
-            }
+            // row[n] += w * (c * ur[n] * sj), c = w- * ul[m]   (and the mirrored RL term)
+            if (do_lr)
+                for (int q = 0; q < nqf; ++q) {
+                    const double ul_m = trace[q * nfn + m], ur_n = uR[q * nfn + n];
+                    lr = __dadd_rn(lr, __dmul_rn(fqw[q], __dmul_rn(__dmul_rn(__dmul_rn(s_wm[q], ul_m), ur_n), s_sj[q])));
+                }
+            if (do_rl)
+                for (int q = 0; q < nqf; ++q) {
+                    const double ur_m = uR[q * nfn + m], ul_n = trace[q * nfn + n];
+                    rl = __dadd_rn(rl, __dmul_rn(fqw[q], __dmul_rn(__dmul_rn(__dmul_rn(s_wp[q], ur_m), ul_n), s_sj[q])));
+                }
             mlr = fmax(mlr, fabs(lr));
             mrl = fmax(mrl, fabs(rl));
         }
