@@ -1002,8 +1002,11 @@ struct Setup {
     std::vector<std::vector<double>> traceR;  // per orientation code: nqf * nfn at mapped point
     // max|LR|, max|RL| per (ordinate, interior face) computed on the device
     // (hsw_setup.cu, bit-identical to the host loop below); empty: host computes
-    std::unique_ptr<double[]> dev_cmax;   // uninitialised storage: the device copy overwrites all of it
-    std::function<void(int)> cmax_wait;   // blocks until ordinate d's block of dev_cmax has arrived
+    // coupling magnitudes from the device (hsw_create's CouplingFeed): acquire blocks until
+    // ordinate d's [nfi][2] block has arrived and returns it, release hands its slot back
+    std::function<const double*(int)> cmax_acquire;
+    std::function<void(int)> cmax_release;
+    std::vector<double> face_len;   // per interior face: sum_q w_q sj_q (assembly.hpp:231)
     // per ordinate
     std::vector<std::vector<Coupling>> couplings;
     std::vector<std::vector<double>> weights;
@@ -1418,7 +1421,21 @@ struct Setup {
             rom_omask.assign((size_t)nd * nel, 0);
             rom_unconverged.assign(nd, 0);
         }
+        if (cmax_acquire) {
+            face_len.assign(nfi, 0.0);
+            parallel_for(nfi, [&](int64_t fi) {
+                const IFace& F = mesh.ifaces[fi];
+                const double* sjv = &fsj[((size_t)F.el * nf + F.fl) * nqf];
+                double length = 0.0;
+                for (int q = 0; q < nqf; ++q) length += fq_w[q] * sjv[q];
+                face_len[fi] = length;
+            });
+        }
+        std::atomic<long long> phase_acc[3];
+        for (auto& a : phase_acc) a.store(0);
+        std::atomic<long long>* phase_us = std::getenv("HSW_SETUP_TIMING") ? phase_acc : nullptr;
         parallel_for(oe - ob, [&](int64_t i64) {
+            const auto t_begin = std::chrono::steady_clock::now();
             const int d = ob + (int)i64;
             const double* om = &odir[3 * d];
             std::vector<double> LR((size_t)nfn * nfn), RL((size_t)nfn * nfn), wp(nqf), wm(nqf);
@@ -1426,7 +1443,7 @@ struct Setup {
             auto& wts = weights[d];
             cpl.reserve((size_t)nfi + nfi / 8);   // about one coupling per interior face
             wts.reserve((size_t)nfi + nfi / 8);
-            if (dev_cmax && cmax_wait) cmax_wait(d);
+            const double* cmax = cmax_acquire ? cmax_acquire(d) : nullptr;   // [nfi][2] of this ordinate
             // Romberg sampling of one face at parameter t (assembly.hpp:103-117): geometry of
             // the (left) element's face, its face-node traces, the neighbour's at t or 1 - t
             std::vector<double> gg((size_t)mesh.npe * dim), full(nb), ul(nfn), ur(nfn), packed, gtmp;
@@ -1520,16 +1537,9 @@ struct Setup {
                 }
                 const double* geo = &fgeom[(((size_t)F.el * nf + F.fl) * nqf) * 4];
                 const double* sjv = &fsj[((size_t)F.el * nf + F.fl) * nqf];
-                std::fill(LR.begin(), LR.end(), 0.0);
-                std::fill(RL.begin(), RL.end(), 0.0);
-                double length = 0.0;
-                const double* uR0 = traceR[F.orient].data();
-                if (dev_cmax) {   // magnitudes from the device; length here
-                    double length = 0.0;
-                    for (int q = 0; q < nqf; ++q) length += fq_w[q] * sjv[q];
-                    const double eps = 1e-12 * length;
-                    const double mlr = dev_cmax[((size_t)(d - ob) * nfi + fi) * 2],
-                                 mrl = dev_cmax[((size_t)(d - ob) * nfi + fi) * 2 + 1];
+                if (cmax) {   // magnitudes from the device; the face length from the shared table
+                    const double eps = 1e-12 * face_len[fi];
+                    const double mlr = cmax[(size_t)fi * 2], mrl = cmax[(size_t)fi * 2 + 1];
                     if (mlr > eps) {
                         cpl.push_back({fi, F.el, F.er, F.fl, F.fr});
                         wts.push_back(weight_of(mlr, F.el, F.fl, LR, false));
@@ -1540,6 +1550,10 @@ struct Setup {
                     }
                     continue;
                 }
+                std::fill(LR.begin(), LR.end(), 0.0);
+                std::fill(RL.begin(), RL.end(), 0.0);
+                double length = 0.0;
+                const double* uR0 = traceR[F.orient].data();
                 for (int q = 0; q < nqf; ++q) {
                     double on = 0.0;
                     for (int k = 0; k < dim; ++k) on += om[k] * geo[q * 4 + k];
@@ -1605,9 +1619,12 @@ struct Setup {
                         for (int m = 0; m < nfn; ++m) dst[m] += mom[m];
                     }
             }
+            if (cmax) cmax_release(d);
+            const auto t_faces = std::chrono::steady_clock::now();
             std::vector<Edge> edges(cpl.size());
             for (size_t c = 0; c < cpl.size(); ++c) edges[c] = {cpl[c].up, cpl[c].down, wts[c]};
             ords[d] = sweep_ordering(nel, edges, fas_thr);
+            const auto t_order = std::chrono::steady_clock::now();
             Ordering& o = ords[d];
             auto& lg = lagged[d];
             lg.assign(cpl.size(), 0);
@@ -1633,7 +1650,17 @@ struct Setup {
                 }
                 o.level[e] = lv;
             }
+            if (phase_us) {   // HSW_SETUP_TIMING: thread-seconds per part, summed over the ordinates
+                const auto t_end = std::chrono::steady_clock::now();
+                auto us = [](auto a, auto b) { return (long long)std::chrono::duration_cast<std::chrono::microseconds>(b - a).count(); };
+                phase_us[0] += us(t_begin, t_faces);
+                phase_us[1] += us(t_faces, t_order);
+                phase_us[2] += us(t_order, t_end);
+            }
         });
+        if (phase_us)
+            std::fprintf(stderr, "  ordinates (thread-seconds): couplings %.3f, sweep_ordering %.3f, lag flags + levels %.3f\n",
+                         phase_us[0].load() * 1e-6, phase_us[1].load() * 1e-6, phase_us[2].load() * 1e-6);
     }
 
     // face -> max|block|; siginvface -> max|M_t^{-1} block| (sweepgraph.hpp:60-72)
@@ -2308,27 +2335,33 @@ void device_init(hsw_handle* h, int device) {
     CUDA_OK(cudaEventCreate(&h->ev1));
 }
 
-// max|LR|, max|RL| of every (ordinate, interior face) on the device, in blocks
-// of ordinates, into S.dev_cmax for Setup::ordinates.  The blocks
-// are produced on a helper thread in ascending ordinate order while Setup::ordinates
-// (whose tasks are claimed in the same order) already works on the finished ones:
-// S.cmax_wait(d) blocks until ordinate d's magnitudes have arrived.
+// max|LR|, max|RL| of every (ordinate, interior face) on the device, in blocks of
+// ordinates, for Setup::ordinates.  The blocks are produced on a helper
+// thread in ascending ordinate order into a small ring of pinned host slots while
+// Setup::ordinates (whose tasks are claimed in the same order) already works on the
+// finished ones: S.cmax_acquire(d) blocks until ordinate d's magnitudes have arrived,
+// S.cmax_release(d) counts the block's slot down; the producer reuses a slot once every
+// ordinate of its previous block has been released.
 struct CouplingFeed {
+    static constexpr int kSlots = 4;
     hsw_handle* h;
     int nfi = 0, chunk = 1, nchunks = 0;
+    size_t slot_doubles = 0;
     int* d_if = nullptr;
     double *d_sj = nullptr, *d_w = nullptr, *d_tr = nullptr, *d_trR = nullptr, *d_od = nullptr;
     double* d_out[2] = {nullptr, nullptr};
+    double* ring = nullptr;   // pinned, kSlots blocks
     cudaStream_t kern = nullptr, copy = nullptr;   // its own streams: the handle's stream builds device state meanwhile
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    std::unique_ptr<std::atomic<int>[]> ready;
-    std::atomic<bool> failed{false};
+    cudaEvent_t ev_t0[2] = {nullptr, nullptr};   // HSW_SETUP_TIMING: kernel start events
+    double kernel_ms = 0.0, wait_slot_ms = 0.0, total_ms = 0.0;
+    std::unique_ptr<std::atomic<int>[]> ready, left;
+    std::atomic<bool> failed{false}, abort{false};
 
     explicit CouplingFeed(hsw_handle* hh) : h(hh) {
         Setup& S = h->S;
         nfi = (int)S.mesh.ifaces.size();
         if (nfi == 0) return;
-        S.dev_cmax.reset(new double[(size_t)(S.oe - S.ob) * nfi * 2]);
         std::vector<int> iface((size_t)nfi * 5);
         for (int i = 0; i < nfi; ++i) {
             const IFace& F = S.mesh.ifaces[i];
@@ -2344,26 +2377,39 @@ struct CouplingFeed {
         d_tr = dev_upload(S.trace);
         d_trR = dev_upload(trR);
         d_od = dev_upload(S.odir);
-        // blocks of about 24 MB of magnitudes (C4: 16 ordinates), two device buffers
-        chunk = std::max(1, std::min(S.oe - S.ob, (int)(std::max<size_t>(1, (size_t)(24u << 20) / ((size_t)nfi * 16)))));
-        nchunks = (S.oe - S.ob + chunk - 1) / chunk;
-        for (auto& b : d_out) CUDA_OK(cudaMalloc(&b, (size_t)chunk * nfi * 2 * sizeof(double)));
+        // blocks of about 12 MB of magnitudes (C4: 8 ordinates), two device buffers
+        const int nds = S.oe - S.ob;
+        chunk = std::max(1, std::min(nds, (int)(std::max<size_t>(1, (size_t)(12u << 20) / ((size_t)nfi * 16)))));
+        nchunks = (nds + chunk - 1) / chunk;
+        slot_doubles = (size_t)chunk * nfi * 2;
+        for (auto& b : d_out) CUDA_OK(cudaMalloc(&b, slot_doubles * sizeof(double)));
+        CUDA_OK(cudaMallocHost(&ring, (size_t)std::min(kSlots, nchunks) * slot_doubles * sizeof(double)));
         CUDA_OK(cudaStreamCreateWithFlags(&kern, cudaStreamNonBlocking));
         CUDA_OK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-        for (auto& e : ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const bool timing = std::getenv("HSW_SETUP_TIMING") != nullptr;
+        for (auto& e : ev) CUDA_OK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+        if (timing)
+            for (auto& e : ev_t0) CUDA_OK(cudaEventCreate(&e));
         ready.reset(new std::atomic<int>[nchunks]);
-        for (int k = 0; k < nchunks; ++k) ready[k].store(0);
-        S.cmax_wait = [this](int d) {
-            const int k = (d - h->S.ob) / chunk;
+        left.reset(new std::atomic<int>[nchunks]);
+        for (int k = 0; k < nchunks; ++k) {
+            ready[k].store(0);
+            left[k].store(std::min(chunk, nds - k * chunk));
+        }
+        S.cmax_acquire = [this](int d) -> const double* {
+            const int i = d - h->S.ob, k = i / chunk;
             while (!ready[k].load(std::memory_order_acquire)) {
                 if (failed.load()) throw hsw::Error(HSW_ERR_CUDA, "hsw_create: the device coupling pass failed");
-                std::this_thread::sleep_for(std::chrono::microseconds(50));
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
             }
+            return ring + (size_t)(k % kSlots) * slot_doubles + (size_t)(i - k * chunk) * nfi * 2;
         };
+        S.cmax_release = [this](int d) { left[(d - h->S.ob) / chunk].fetch_sub(1, std::memory_order_release); };
     }
     void launch(int k) {
         Setup& S = h->S;
         const int d0 = S.ob + k * chunk, d1 = std::min(S.oe, d0 + chunk);
+        if (ev_t0[k & 1]) CUDA_OK(cudaEventRecord(ev_t0[k & 1], kern));
         dev_coupling_max(S.dim, nfi, S.nf, S.nqf, S.nfn, d_if, h->d_fgeom, d_sj, d_w, d_tr, d_trR, d_od, d0, d1,
                          d_out[k & 1], kern);
         CUDA_OK(cudaEventRecord(ev[k & 1], kern));
@@ -2373,32 +2419,52 @@ struct CouplingFeed {
         try {
             Setup& S = h->S;
             CUDA_OK(cudaSetDevice(h->device));
+            const auto t_begin = std::chrono::steady_clock::now();
             launch(0);
             for (int k = 0; k < nchunks; ++k) {
-                // block k + 1 is computed while block k is copied (its buffer was drained
-                // by the synchronous copy of block k - 1)
+                // block k + 1 is computed while block k is copied (its device buffer was
+                // drained by the completed copy of block k - 1)
                 if (k + 1 < nchunks) launch(k + 1);
+                const auto t_w = std::chrono::steady_clock::now();
+                while (k >= kSlots && left[k - kSlots].load(std::memory_order_acquire) > 0) {
+                    if (abort.load()) return;   // the consumers are gone (an ordinate task threw)
+                    std::this_thread::sleep_for(std::chrono::microseconds(20));
+                }
+                wait_slot_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_w).count();
                 const int d0 = S.ob + k * chunk, d1 = std::min(S.oe, d0 + chunk);
                 CUDA_OK(cudaStreamWaitEvent(copy, ev[k & 1], 0));
-                CUDA_OK(cudaMemcpyAsync(&S.dev_cmax[(size_t)(d0 - S.ob) * nfi * 2], d_out[k & 1],
+                CUDA_OK(cudaMemcpyAsync(ring + (size_t)(k % kSlots) * slot_doubles, d_out[k & 1],
                                         (size_t)(d1 - d0) * nfi * 2 * sizeof(double), cudaMemcpyDeviceToHost, copy));
                 CUDA_OK(cudaStreamSynchronize(copy));
+                if (ev_t0[k & 1]) {
+                    float ms = 0.f;
+                    CUDA_OK(cudaEventElapsedTime(&ms, ev_t0[k & 1], ev[k & 1]));
+                    kernel_ms += ms;
+                }
                 ready[k].store(1, std::memory_order_release);
             }
+            total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+            if (ev_t0[0])
+                std::fprintf(stderr, "  coupling feed: %d blocks of %d ordinates, kernels %.1f ms, waited for slots %.1f ms, "
+                             "producer %.1f ms\n", nchunks, chunk, kernel_ms, wait_slot_ms, total_ms);
         } catch (...) {
             failed.store(true);
             throw;
         }
     }
     ~CouplingFeed() {
-        h->S.cmax_wait = nullptr;
+        h->S.cmax_acquire = nullptr;
+        h->S.cmax_release = nullptr;
         if (kern) cudaStreamSynchronize(kern);
         for (void* b : {(void*)d_if, (void*)d_sj, (void*)d_w, (void*)d_tr, (void*)d_trR, (void*)d_od, (void*)d_out[0],
                         (void*)d_out[1]})
             cudaFree(b);
+        if (ring) cudaFreeHost(ring);
         if (kern) cudaStreamDestroy(kern);
         if (copy) cudaStreamDestroy(copy);
         for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto e : ev_t0)
             if (e) cudaEventDestroy(e);
     }
 };
@@ -2573,6 +2639,10 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             phase("coupling uploads");
             Async cpl([&] { if (feed) feed->produce(); });
             Async dev(device_static);
+            struct AbortOnExit {   // destroyed before the threads are joined: frees a producer
+                CouplingFeed* f;   // waiting for slots nobody will release (a task threw)
+                ~AbortOnExit() { if (f) f->abort.store(true); }
+            } abort_guard{feed.get()};
             S.ordinates();
             phase("ordinates");
             S.worklists();
@@ -2581,7 +2651,6 @@ int hsw_create(const hsw_problem_desc* desc, hsw_handle** out) {
             dev.join();
             phase("device state");
         }
-        S.dev_cmax.reset();
         h->d_inflags = dev_upload(S.inflags);
         h->d_pairs_all = dev_upload(S.pairs_all);
         h->d_pairs_dir = dev_upload(S.pairs_dir);
